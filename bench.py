@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark: constructed tours/sec at pr2392 (ACS, 2392 ants, cl=32, k=1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--variant atomic]
+    python bench.py --impl reference ...      # CPU reference arm (oracle port, all host threads)
+
+One step = one ACS iteration of the colony: m = n = 2392 tours constructed
+(warp per ant, whole tour per launch), iteration best, global-best update.
+Under torchrun (N > 1) every rank runs its own colony on its own GPU (island
+model); colonies exchange the global best through NCCL every
+--exchange-every iterations inside the timed region.  value = all tours built
+by all ranks / max over ranks of the device time.  L2 is flushed (256 MiB
+write) before every timed step; each step is timed with CUDA events on the
+colony stream (acs_gpu_last_timing).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "constructed tours/sec at pr2392 (1/2/4/8 B200); mean % over optimum"
+PAPER_ACS_GPU_PR2392 = 4942.0  # ACS-GPU (atomic) pr2392, GK104
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--instance", default="pr2392")
+    ap.add_argument("--variant", default="atomic")
+    ap.add_argument("--ants", type=int, default=0)
+    ap.add_argument("--k", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--exchange-every", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_bytes_per_tour(n: int, L: int, k: int, variant: str, slots: int = 8) -> int:
+    """B = n*(cl*(4+S) + 4) + ceil(n/k)*4S (dense) with S = 8;
+    selective: n*(cl*(4+S) + s*(4+S) + 8) + ceil(n/k)*2*(s*4 + S + 4).
+    The fallback term F is added from the device counter by the caller."""
+    S = 8
+    upd = -(-n // k)
+    if variant in ("spm", "spm-seq"):
+        return n * (L * (4 + S) + slots * (4 + S) + 8) + upd * 2 * (slots * 4 + S + 4)
+    return n * (L * (4 + S) + 4) + upd * 4 * S
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def ncu_traffic(variant: str):
+    """dram bytes per construct launch from the committed ncu --set full capture."""
+    path = os.path.join(REPO, "profiles", "ncu_construct_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(variant, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_baseline_seq(name: str, m: int, k: int):
+    """oracle SEQ (ACS-SEQ restated) on one host core, bounded sample."""
+    import oracle as O
+    I = O.load(name)
+    iters = 3
+    o = O.Oracle().run(I, m=m, iterations=iters, seed=0, mode=O.SEQ, k=k, want_routes=False)
+    tps = m * iters / (o["loop_ms"] / 1e3)
+    return {"value": round(tps, 1), "unit": "tours/s", "cores": 1, "kind": "port",
+            "sample": f"oracle SEQ (ant-major, immediate updates) on {name}, m={m}, k={k}, "
+                      f"{iters} iterations = {m * iters} tours, {o['loop_ms'] / 1e3:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU port of the reference path on all host threads."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+    I = O.load(args.instance)
+    m = args.ants or I.n
+    threads = os.cpu_count() or 1
+    mode = O.SEQ if args.variant in ("seq", "spm-seq") else (O.SYNC if args.variant == "deferred" else O.RELAXED)
+    memory = O.SELECTIVE if args.variant in ("spm", "spm-seq") else O.DENSE
+    consistent = 1 if args.variant == "atomic" else 0
+    orc = O.Oracle()
+    # warmup + timed steps, one iteration each (the oracle keeps no state across calls,
+    # so each step is a fresh single-iteration colony: same per-iteration work)
+    for _ in range(args.warmup):
+        orc.run(I, m=m, iterations=1, seed=args.seed, mode=mode, memory=memory, consistent=consistent,
+                threads=threads, k=args.k, want_routes=False)
+    loop_ms = []
+    for s in range(args.steps):
+        o = orc.run(I, m=m, iterations=1, seed=args.seed + s, mode=mode, memory=memory,
+                    consistent=consistent, threads=threads, k=args.k, want_routes=False)
+        loop_ms.append(o["loop_ms"])
+    total_s = sum(loop_ms) / 1e3
+    value = m * args.steps / total_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "tours/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(sum(loop_ms) / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": f"TSPLIB {args.instance} (real instance)",
+        "config": {"workload": f"{args.instance} ACS, {m} ants, cl=32, k={args.k}, {args.variant}",
+                   "variant": args.variant, "mode": ["seq", "sync", "relaxed"][mode],
+                   "memory": ["dense", "selective"][memory], "consistent": consistent},
+        "cpu_baseline": {"value": round(value, 1), "unit": "tours/s", "cores": threads, "kind": "port",
+                         "sample": f"oracle/acs_oracle.c OpenMP on {threads} host threads, "
+                                   f"{args.steps} iterations x {m} tours"},
+        "e2e": {"value": round(value, 1), "unit": "tours/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    rank, world, local = dist_env()
+    import numpy as np
+    import torch
+    import oracle as O  # data files + optimum catalog only (no oracle compute here)
+    import paper_1605_02669_b200 as P
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    I = O.load(args.instance)
+    opt = O.optima().get(args.instance)
+    inst = P.TspInstance(I.name, I.type, I.xs.copy(), I.ys.copy(), opt)
+    m = args.ants or inst.n
+    # P11: colony c uses seed + c * golden -> colony 0 == the single-GPU run
+    seed = (args.seed + rank * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+    params = P.AcsParams(variant=args.variant, m=m, k=args.k, seed=seed)
+    col = P.Colony(inst, params, device=local)
+    if world > 1:
+        uid = [P.Colony.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        col.island_init(uid[0], world, rank)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    launches_per_iter = 2 if args.variant != "deferred" else 3 + (inst.n - 1) + (inst.n - 1) // args.k
+
+    def step(i):
+        flush.fill_(i & 0xFF)  # evict L2 (126 MB) before the step
+        torch.cuda.synchronize()
+        col.iterate(1)
+        tot, con = col.last_timing()
+        ex = 0
+        if world > 1 and (i + 1) % args.exchange_every == 0:
+            t0 = time.perf_counter()
+            col.island_exchange()
+            ex = (time.perf_counter() - t0) * 1e3
+        return tot + ex, con
+
+    for i in range(args.warmup):
+        step(i)
+    c0 = col.counters()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        per = [step(args.warmup + i) for i in range(args.steps)]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    c1 = col.counters()
+    total_ms = sum(p[0] for p in per)
+    construct_ms = sum(p[1] for p in per)
+    if dist:
+        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * m * args.steps / (total_ms / 1e3)
+    order, best_len = col.best()
+
+    # roofline of the dominant kernel (construction): algorithmic bytes / launch time
+    fb_elems = c1.get("fallback_elems", 0) - c0.get("fallback_elems", 0)
+    B_tour = algorithmic_bytes_per_tour(inst.n, col.info.list_len, args.k, args.variant)
+    alg_bytes_launch = B_tour * m + fb_elems * 12 / max(args.steps, 1)
+    construct_s = construct_ms / 1e3 / args.steps
+    peaks, src = measured_peaks()
+    achieved = alg_bytes_launch / construct_s / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic(args.variant),
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
+                "kernel": "k_construct_dense" if args.variant != "spm" else "k_construct_spm",
+                "construct_ms_per_launch": round(construct_s * 1e3, 4),
+                "bytes_per_tour": B_tour,
+                "note": "latency-bound dependent-load chain; L2-resident working set"}
+
+    col.close()
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tours/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": round(value / PAPER_ACS_GPU_PR2392, 2) if args.instance == "pr2392" and args.variant == "atomic" else None,
+        "vs_baseline_ref": "paper ACS-GPU (atomic) pr2392 4942 tours/s on GK104 (BASELINE.md, PAPER.md:920)",
+        "dtype": "f64", "data": f"TSPLIB {args.instance} (real instance, data/tsplib)",
+        "config": {"workload": f"{args.instance} ACS, {m} ants, cl=32, k={args.k}, {args.variant} dense"
+                   if args.variant != "spm" else f"{args.instance} ACS-SPM, {m} ants, s=8",
+                   "instance": args.instance, "n": inst.n, "ants_per_gpu": m, "variant": args.variant,
+                   "cl": 32, "k": args.k, "beta": 3.0, "alpha": 0.2, "rho": 0.01,
+                   "q0": round(col.info.q0, 6), "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": f"island x{world}" if world > 1 else "single colony",
+                   "exchange_every": args.exchange_every if world > 1 else None},
+        "roofline": roofline,
+        "gpu_launches": launches_per_iter * args.steps,
+        "clocks": clk.summary(),
+        "quality": {"best_len": int(best_len), "optimum": opt,
+                    "pct_over_opt": round(100.0 * (best_len - opt) / opt, 3) if opt else None,
+                    "iterations": args.warmup + args.steps, "seeds": 1,
+                    "note": "single run; 30-seed study in profiles/quality_*.json"},
+    }
+    if rank == 0 and not args.no_e2e:
+        line["e2e"] = e2e(P, inst, params, args, world)
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_seq(args.instance, m, args.k)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def e2e(P, inst, params, args, world):
+    """Same metric through the public one-call API (acs_gpu_run): host coords in,
+    host best tour + trace out, setup + K iterations inside the timed region."""
+    import ctypes as C
+    import numpy as np
+    from paper_1605_02669_b200 import _native as N
+    K = args.steps
+    d = inst.desc()
+    p = params.to_c(inst.n)
+    order = np.empty(inst.n, np.uint32)
+    trace = np.empty(K, np.int64)
+    bl = C.c_int64()
+    lib = N.lib()
+    t0 = time.perf_counter()
+    N.check(lib.acs_gpu_run(C.byref(d), C.byref(p), K, 0, order.ctypes.data_as(C.c_void_p), C.byref(bl),
+                            trace.ctypes.data_as(C.c_void_p)), "acs_gpu_run")
+    dt = time.perf_counter() - t0
+    m = p.ants
+    return {"value": round(m * K / dt, 1), "unit": "tours/s",
+            "h2d_bytes_per_step": round(2 * 8 * inst.n / K, 1),
+            "d2h_bytes_per_step": round((4 * inst.n + 8) / K + 8, 1),
+            "api": "acs_gpu_run (create + K iterations + best tour/trace D2H + destroy), 1 GPU",
+            "wall_s": round(dt, 4)}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

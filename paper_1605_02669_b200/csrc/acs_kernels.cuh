@@ -1,0 +1,113 @@
+// acs_kernels.cuh -- device-side data layout of one colony and the host
+// launchers of every sm_100a kernel (implemented in acs_kernels.cu).
+//
+// HBM / L2 layout:
+//   rows   n x 32 uint4   per candidate slot: {id | mirror<<24, dist, eta^beta (f64)}
+//                         -- immutable, one coalesced 512 B row per step
+//   tauc   n x 32 f64     pheromone of the candidate edges, candidate order
+//   tau    n x n  f64     dense pheromone matrix (fallback + non-candidate edges)
+//   spm    n x S u32 ids, n x S f64 vals, n u32 tail  (selective memory)
+//   dist   n x n  i32     distance table (n <= 4096, as tsp_instance.hpp:31)
+//   routes m x n  u32, lens m i64
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace acs_dev {
+
+struct DevInstance {
+    uint32_t n, words;   // words = ceil(n/32) visited-bitmask words
+    int type;            // acs_edge_weight
+    const double *xs, *ys;
+    const int32_t *dist; // n*n or nullptr (on-the-fly above 4096 nodes)
+};
+
+struct DevColony {
+    uint32_t m, L, k, S;   // ants, list length, update period, spm slots
+    double q0, beta;
+    int beta_int;          // >=0: integral beta (repeated multiply), -1: pow
+    double c_l, c_0;       // local update tau' = c_l*tau + c_0
+    double tau_min;
+    uint64_t seed;
+    const uint4 *rows;     // n*32 packed candidate rows
+    double *tau;           // n*n dense, or nullptr
+    double *tauc;          // n*32, or nullptr
+    uint32_t *spm_ids;     // n*S
+    double *spm_vals;      // n*S
+    uint32_t *spm_tail;    // n
+    uint32_t *routes;      // m*n
+    int64_t *lens;         // m
+    unsigned long long *counters;  // [8], see Counter
+    const uint64_t *iter;  // device iteration counter (RNG derivation index)
+};
+
+enum Counter {
+    kCntUpdates = 0, kCntHits, kCntMisses, kCntFallback, kCntGreedy, kCntRoulette,
+    kCntCasRetry, kCntIters, kCntFallbackElems, kNumCounters = 16
+};
+
+struct DevBest {
+    uint32_t *tour;        // n
+    int64_t *len;          // 1 (INT64_MAX = none yet)
+    double alpha, c_g;     // global update: tau' = c_g*tau + alpha*(1/L_gb)
+    uint64_t *iter;        // incremented by the epilogue
+    void *stats;           // acs_iter_stats[capacity]
+};
+
+// per-ant state of the step-synchronous (deferred) variant
+struct DevDeferred {
+    uint32_t *cur, *start;
+    uint32_t *vis;         // m * words
+    void *rng;             // m engines (Xoshiro or Philox)
+    uint4 *pend;           // m: {u, v, pos | mirror<<8, due}
+};
+
+// ---- setup launchers (stream-ordered, async) ----
+void launch_distance_table(const DevInstance &I, int32_t *out, cudaStream_t s);
+void launch_topk(const DevInstance &I, uint32_t L, uint32_t *out, cudaStream_t s);
+void launch_build_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, double beta,
+                       int beta_int, uint4 *rows, cudaStream_t s);
+void launch_nn_tour(const DevInstance &I, uint32_t start, int64_t *out, cudaStream_t s);
+void launch_tour_lengths(const DevInstance &I, const uint32_t *routes, uint32_t m, int64_t *out,
+                         cudaStream_t s);
+void launch_fill(double *p, size_t count, double value, cudaStream_t s);
+void launch_spm_init(uint32_t *ids, double *vals, uint32_t *tail, uint32_t n, uint32_t S,
+                     double tau_min, cudaStream_t s);
+void launch_rng_script(uint32_t kind, uint64_t seed, uint64_t it, uint64_t ant, int derive,
+                       const int32_t *ops, const uint64_t *args, uint64_t *out, uint32_t count,
+                       cudaStream_t s);
+void launch_spm_script(uint32_t *ids, double *vals, uint32_t *tail, uint32_t S, double tau_min,
+                       double c_l, double c_0, double alpha, double c_g, const uint32_t *ops,
+                       const int64_t *lgb, uint32_t count, double *out,
+                       unsigned long long *hits_misses, cudaStream_t s);
+
+// ---- per-iteration launchers ----
+// variant: 0 atomic, 2 relaxed, 3 spm, 4 seq (dense, 1 warp), 5 spm seq (1 warp)
+void launch_construct(int variant, int rng, const DevInstance &I, const DevColony &C,
+                      cudaStream_t s);
+// deferred (SYNC) variant: init, n-1 x (select, apply), close
+void launch_deferred_init(int rng, const DevInstance &I, const DevColony &C,
+                          const DevDeferred &D, cudaStream_t s);
+void launch_deferred_select(int rng, const DevInstance &I, const DevColony &C,
+                            const DevDeferred &D, uint32_t step, cudaStream_t s);
+void launch_deferred_apply(const DevInstance &I, const DevColony &C, const DevDeferred &D,
+                           cudaStream_t s);
+void launch_deferred_close(const DevInstance &I, const DevColony &C, const DevDeferred &D,
+                           cudaStream_t s);
+// eval-free epilogue: iteration best (ties lowest ant), strict global best,
+// global update on the best tour, stats[slot], iter++
+void launch_epilogue(bool spm, const DevInstance &I, const DevColony &C, const DevBest &B,
+                     uint32_t slot, cudaStream_t s);
+// island import: adopt (tour,len) from device buffers if strictly better
+void launch_adopt_best(const uint32_t *tour, const int64_t *len, const DevInstance &I,
+                       const DevBest &B, cudaStream_t s);
+
+size_t deferred_rng_bytes(int rng);
+
+// island exchange helpers
+void launch_island_pack(const int64_t *best_len, int rank, int64_t *key, cudaStream_t s);
+void launch_island_mask(const int64_t *key, int rank, const uint32_t *best_tour, uint32_t n,
+                        uint32_t *x_tour, int64_t *x_len, cudaStream_t s);
+
+}  // namespace acs_dev

@@ -1,0 +1,728 @@
+// capi.cu -- extern "C" entry points of include/acs_gpu.h: the drop-in
+// boundary of the B200 ACS hot path.  Contexts own all device memory; every
+// compute call is stream-ordered on the context stream and synchronises only
+// where the ABI hands results back to the host.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/acs_gpu.h"
+#include "acs_kernels.cuh"
+
+using namespace acs_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+    do {                                                                                \
+        const cudaError_t e_ = (expr);                                                  \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(e_ == cudaErrorMemoryAllocation ? ACS_E_NOMEM : ACS_E_CUDA,      \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+// device buffer with RAII
+template <class T>
+struct DBuf {
+    T *p = nullptr;
+    size_t count = 0;
+    DBuf() = default;
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        count = 0;
+    }
+    cudaError_t alloc(size_t n) {
+        release();
+        count = n;
+        return n ? cudaMalloc(reinterpret_cast<void **>(&p), n * sizeof(T)) : cudaSuccess;
+    }
+    size_t bytes() const { return count * sizeof(T); }
+};
+
+int check_instance(const acs_instance_desc *inst) {
+    if (!inst || !inst->xs || !inst->ys) return fail(ACS_E_ARG, "instance: null pointer");
+    if (inst->n < 3) return fail(ACS_E_ARG, "instance needs at least 3 nodes, got " + std::to_string(inst->n));
+    if (inst->n > 0x00FFFFFEu) return fail(ACS_E_ARG, "instance: n exceeds 2^24-2 nodes");
+    if (inst->edge_weight_type > ACS_ATT) return fail(ACS_E_ARG, "instance: unknown edge weight type");
+    return ACS_OK;
+}
+
+int set_device(int device) {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(ACS_E_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= count) return fail(ACS_E_ARG, "device index out of range");
+    CUDA_TRY(cudaSetDevice(device));
+    return ACS_OK;
+}
+
+// instance coordinates resident on the device (+ distance table when n <= 4096)
+struct DevInst {
+    DBuf<double> xs, ys;
+    DBuf<int32_t> dist;
+    DevInstance view{};
+
+    int upload(const acs_instance_desc *inst, bool want_table, cudaStream_t s) {
+        const uint32_t n = inst->n;
+        CUDA_TRY(xs.alloc(n));
+        CUDA_TRY(ys.alloc(n));
+        CUDA_TRY(cudaMemcpyAsync(xs.p, inst->xs, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(ys.p, inst->ys, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        view.n = n;
+        view.words = (n + 31) / 32;
+        view.type = static_cast<int>(inst->edge_weight_type);
+        view.xs = xs.p;
+        view.ys = ys.p;
+        view.dist = nullptr;
+        if (want_table && n <= 4096) {  // tsp_instance.hpp:31 kDistTableMaxNodes
+            CUDA_TRY(dist.alloc(static_cast<size_t>(n) * n));
+            launch_distance_table(view, dist.p, s);
+            CUDA_TRY(cudaGetLastError());
+            view.dist = dist.p;
+        }
+        return ACS_OK;
+    }
+};
+
+struct Stream {
+    cudaStream_t s = nullptr;
+    ~Stream() {
+        if (s) cudaStreamDestroy(s);
+    }
+    int create() {
+        CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        return ACS_OK;
+    }
+};
+
+int beta_int_of(double beta) {
+    return (beta >= 0.0 && beta <= 64.0 && beta == std::floor(beta)) ? static_cast<int>(beta) : -1;
+}
+
+double default_q0(uint32_t n) { return n <= 20 ? 0.0 : static_cast<double>(n - 20) / static_cast<double>(n); }
+
+// ---- lazily loaded NCCL (island model) ----
+typedef struct { char internal[128]; } nccl_uid;
+typedef void *nccl_comm;
+struct NcclApi {
+    void *h = nullptr;
+    int (*get_unique_id)(nccl_uid *) = nullptr;
+    int (*comm_init_rank)(nccl_comm *, int, nccl_uid, int) = nullptr;
+    int (*comm_destroy)(nccl_comm) = nullptr;
+    int (*all_reduce)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+    int (*broadcast)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+    const char *(*error_string)(int) = nullptr;
+
+    int load() {
+        if (h) return ACS_OK;
+        const char *names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char *nm : names) {
+            h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) return fail(ACS_E_NCCL, "libnccl.so.2 not loadable");
+        get_unique_id = reinterpret_cast<decltype(get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        comm_init_rank = reinterpret_cast<decltype(comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        comm_destroy = reinterpret_cast<decltype(comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        all_reduce = reinterpret_cast<decltype(all_reduce)>(dlsym(h, "ncclAllReduce"));
+        broadcast = reinterpret_cast<decltype(broadcast)>(dlsym(h, "ncclBroadcast"));
+        error_string = reinterpret_cast<decltype(error_string)>(dlsym(h, "ncclGetErrorString"));
+        if (!get_unique_id || !comm_init_rank || !comm_destroy || !all_reduce || !broadcast)
+            return fail(ACS_E_NCCL, "libnccl: missing symbols");
+        return ACS_OK;
+    }
+};
+NcclApi g_nccl;
+constexpr int kNcclInt64 = 4, kNcclUint32 = 3, kNcclMin = 3, kNcclSum = 0;
+
+}  // namespace
+
+void acs_set_error(const char *msg) { g_err = msg ? msg : ""; }
+
+struct acs_gpu_ctx {
+    int device = 0;
+    Stream stream;
+    acs_params params{};
+    DevInst inst;
+    uint32_t n = 0, m = 0, L = 0, S = 0;
+    double q0 = 0, tau0 = 0;
+    int64_t nn_len = 0;
+    DBuf<uint4> rows;
+    DBuf<uint32_t> cand;  // flat n*L (reference layout), kept for get_candidates
+    DBuf<double> tau, tauc, spm_vals;
+    DBuf<uint32_t> spm_ids, spm_tail, routes, best_tour;
+    DBuf<int64_t> lens, best_len;
+    DBuf<uint64_t> iter;
+    DBuf<unsigned long long> counters;
+    DBuf<acs_iter_stats> stats;
+    // deferred variant state
+    DBuf<uint32_t> d_cur, d_start, d_vis;
+    DBuf<unsigned char> d_rng;
+    DBuf<uint4> d_pend;
+    // island exchange scratch
+    DBuf<int64_t> x_key;
+    DBuf<uint32_t> x_tour;
+    DBuf<int64_t> x_len;
+    nccl_comm comm = nullptr;
+    int rank = 0, nranks = 1;
+    // timing
+    std::vector<cudaEvent_t> events;
+    float last_total_ms = 0, last_construct_ms = 0;
+    DevColony colony{};
+    DevBest best{};
+    DevDeferred deferred{};
+
+    ~acs_gpu_ctx() {
+        if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
+    }
+    bool dense() const { return params.variant != ACS_VARIANT_SPM && params.variant != ACS_VARIANT_SPM_SEQ; }
+    int ensure_events(size_t count) {
+        while (events.size() < count) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreate(&e));
+            events.push_back(e);
+        }
+        return ACS_OK;
+    }
+    size_t device_bytes() const {
+        return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + rows.bytes() + cand.bytes() +
+               tau.bytes() + tauc.bytes() + spm_vals.bytes() + spm_ids.bytes() + spm_tail.bytes() +
+               routes.bytes() + best_tour.bytes() + lens.bytes() + d_vis.bytes() + d_rng.bytes() +
+               d_pend.bytes() + d_cur.bytes() + d_start.bytes();
+    }
+};
+
+extern "C" {
+
+const char *acs_gpu_last_error(void) { return g_err.c_str(); }
+int acs_gpu_abi_version(void) { return ACS_GPU_ABI_VERSION; }
+
+int acs_gpu_device_count(int *count) {
+    if (!count) return fail(ACS_E_ARG, "null count");
+    *count = 0;
+    const cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return fail(ACS_E_CUDA, cudaGetErrorString(e));
+    }
+    return ACS_OK;
+}
+
+int acs_gpu_distance_table(const acs_instance_desc *inst, int device, int32_t *out) {
+    if (int rc = check_instance(inst)) return rc;
+    if (!out) return fail(ACS_E_ARG, "null output");
+    if (int rc = set_device(device)) return rc;
+    Stream st;
+    if (int rc = st.create()) return rc;
+    DevInst di;
+    if (int rc = di.upload(inst, false, st.s)) return rc;
+    DBuf<int32_t> d;
+    CUDA_TRY(d.alloc(static_cast<size_t>(inst->n) * inst->n));
+    launch_distance_table(di.view, d.p, st.s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, d.p, d.bytes(), cudaMemcpyDeviceToHost, st.s));
+    CUDA_TRY(cudaStreamSynchronize(st.s));
+    return ACS_OK;
+}
+
+int acs_gpu_build_candidates(const acs_instance_desc *inst, uint32_t cl, int device,
+                             uint32_t *out_flat, uint32_t *list_len) {
+    if (int rc = check_instance(inst)) return rc;
+    if (cl < 1 || cl > 32) return fail(ACS_E_ARG, "cl must be in [1, 32] on the GPU path");
+    const uint32_t L = cl < inst->n - 1 ? cl : inst->n - 1;
+    if (list_len) *list_len = L;
+    if (!out_flat) return ACS_OK;
+    if (int rc = set_device(device)) return rc;
+    Stream st;
+    if (int rc = st.create()) return rc;
+    DevInst di;
+    if (int rc = di.upload(inst, false, st.s)) return rc;
+    DBuf<uint32_t> d;
+    CUDA_TRY(d.alloc(static_cast<size_t>(inst->n) * L));
+    launch_topk(di.view, L, d.p, st.s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out_flat, d.p, d.bytes(), cudaMemcpyDeviceToHost, st.s));
+    CUDA_TRY(cudaStreamSynchronize(st.s));
+    return ACS_OK;
+}
+
+int acs_gpu_nn_tour_length(const acs_instance_desc *inst, uint32_t start, int device, int64_t *out) {
+    if (int rc = check_instance(inst)) return rc;
+    if (!out || start >= inst->n) return fail(ACS_E_ARG, "bad start / null output");
+    if (int rc = set_device(device)) return rc;
+    Stream st;
+    if (int rc = st.create()) return rc;
+    DevInst di;
+    if (int rc = di.upload(inst, true, st.s)) return rc;
+    DBuf<int64_t> d;
+    CUDA_TRY(d.alloc(1));
+    launch_nn_tour(di.view, start, d.p, st.s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, d.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st.s));
+    CUDA_TRY(cudaStreamSynchronize(st.s));
+    return ACS_OK;
+}
+
+int acs_gpu_tour_lengths(const acs_instance_desc *inst, const uint32_t *routes, uint32_t m,
+                         int device, int64_t *out) {
+    if (int rc = check_instance(inst)) return rc;
+    if (!routes || !out || m == 0) return fail(ACS_E_ARG, "null routes/output or m == 0");
+    if (int rc = set_device(device)) return rc;
+    Stream st;
+    if (int rc = st.create()) return rc;
+    DevInst di;
+    if (int rc = di.upload(inst, true, st.s)) return rc;
+    DBuf<uint32_t> r;
+    DBuf<int64_t> d;
+    CUDA_TRY(r.alloc(static_cast<size_t>(m) * inst->n));
+    CUDA_TRY(d.alloc(m));
+    CUDA_TRY(cudaMemcpyAsync(r.p, routes, r.bytes(), cudaMemcpyHostToDevice, st.s));
+    launch_tour_lengths(di.view, r.p, m, d.p, st.s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, d.p, d.bytes(), cudaMemcpyDeviceToHost, st.s));
+    CUDA_TRY(cudaStreamSynchronize(st.s));
+    return ACS_OK;
+}
+
+int acs_gpu_rng_script(uint32_t kind, uint64_t seed, uint64_t iteration, uint64_t ant, int derive,
+                       const int32_t *ops, const uint64_t *args, uint64_t *out, uint32_t count,
+                       int device) {
+    if (!ops || !out || count == 0) return fail(ACS_E_ARG, "null ops/out or empty script");
+    if (kind > ACS_RNG_PHILOX) return fail(ACS_E_ARG, "unknown rng kind");
+    if (int rc = set_device(device)) return rc;
+    Stream st;
+    if (int rc = st.create()) return rc;
+    DBuf<int32_t> o;
+    DBuf<uint64_t> a, r;
+    CUDA_TRY(o.alloc(count));
+    CUDA_TRY(a.alloc(count));
+    CUDA_TRY(r.alloc(count));
+    CUDA_TRY(cudaMemcpyAsync(o.p, ops, o.bytes(), cudaMemcpyHostToDevice, st.s));
+    if (args) CUDA_TRY(cudaMemcpyAsync(a.p, args, a.bytes(), cudaMemcpyHostToDevice, st.s));
+    else CUDA_TRY(cudaMemsetAsync(a.p, 0, a.bytes(), st.s));
+    launch_rng_script(kind, seed, iteration, ant, derive, o.p, a.p, r.p, count, st.s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, r.p, r.bytes(), cudaMemcpyDeviceToHost, st.s));
+    CUDA_TRY(cudaStreamSynchronize(st.s));
+    return ACS_OK;
+}
+
+int acs_gpu_spm_script(uint32_t n, uint32_t slots, double tau_min, double rho, double tau0,
+                       double alpha, const uint32_t *ops, const int64_t *l_gb, uint32_t count,
+                       int device, double *out, uint32_t *ids, double *vals, uint32_t *tail,
+                       uint64_t *hits, uint64_t *misses) {
+    if (n == 0 || slots == 0 || !ops || count == 0) return fail(ACS_E_ARG, "bad spm script");
+    for (uint32_t i = 0; i < count; ++i) {
+        if (ops[3 * i] >= n || ops[3 * i + 1] >= n || ops[3 * i + 2] > 2)
+            return fail(ACS_E_ARG, "spm script op out of range");
+        if (ops[3 * i + 2] == 1 && (!l_gb || l_gb[i] <= 0)) return fail(ACS_E_ARG, "global op needs l_gb > 0");
+    }
+    if (int rc = set_device(device)) return rc;
+    Stream st;
+    if (int rc = st.create()) return rc;
+    DBuf<uint32_t> did, dtail, dops;
+    DBuf<double> dvals, dout;
+    DBuf<int64_t> dl;
+    DBuf<unsigned long long> hm;
+    CUDA_TRY(did.alloc(static_cast<size_t>(n) * slots));
+    CUDA_TRY(dvals.alloc(static_cast<size_t>(n) * slots));
+    CUDA_TRY(dtail.alloc(n));
+    CUDA_TRY(dops.alloc(3ull * count));
+    CUDA_TRY(dout.alloc(count));
+    CUDA_TRY(dl.alloc(count));
+    CUDA_TRY(hm.alloc(2));
+    launch_spm_init(did.p, dvals.p, dtail.p, n, slots, tau_min, st.s);
+    CUDA_TRY(cudaMemcpyAsync(dops.p, ops, dops.bytes(), cudaMemcpyHostToDevice, st.s));
+    if (l_gb) CUDA_TRY(cudaMemcpyAsync(dl.p, l_gb, dl.bytes(), cudaMemcpyHostToDevice, st.s));
+    else CUDA_TRY(cudaMemsetAsync(dl.p, 0, dl.bytes(), st.s));
+    CUDA_TRY(cudaMemsetAsync(hm.p, 0, hm.bytes(), st.s));
+    const double c_l = 1.0 - rho, c_0 = rho * tau0, c_g = 1.0 - alpha;
+    launch_spm_script(did.p, dvals.p, dtail.p, slots, tau_min, c_l, c_0, alpha, c_g, dops.p, dl.p,
+                      count, dout.p, hm.p, st.s);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long h[2] = {0, 0};
+    if (out) CUDA_TRY(cudaMemcpyAsync(out, dout.p, dout.bytes(), cudaMemcpyDeviceToHost, st.s));
+    if (ids) CUDA_TRY(cudaMemcpyAsync(ids, did.p, did.bytes(), cudaMemcpyDeviceToHost, st.s));
+    if (vals) CUDA_TRY(cudaMemcpyAsync(vals, dvals.p, dvals.bytes(), cudaMemcpyDeviceToHost, st.s));
+    if (tail) CUDA_TRY(cudaMemcpyAsync(tail, dtail.p, dtail.bytes(), cudaMemcpyDeviceToHost, st.s));
+    CUDA_TRY(cudaMemcpyAsync(h, hm.p, sizeof(h), cudaMemcpyDeviceToHost, st.s));
+    CUDA_TRY(cudaStreamSynchronize(st.s));
+    if (hits) *hits = h[0];
+    if (misses) *misses = h[1];
+    return ACS_OK;
+}
+
+int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int device, acs_gpu_ctx **out) {
+    if (!out) return fail(ACS_E_ARG, "null ctx output");
+    *out = nullptr;
+    if (int rc = check_instance(inst)) return rc;
+    if (!p) return fail(ACS_E_ARG, "null params");
+    if (p->cl < 1 || p->cl > 32) return fail(ACS_E_ARG, "cl must be in [1, 32] on the GPU path");
+    if (p->update_period < 1) return fail(ACS_E_ARG, "update_period (k) must be >= 1");
+    if (p->variant > ACS_VARIANT_SPM_SEQ) return fail(ACS_E_ARG, "unknown variant");
+    if (p->rng > ACS_RNG_PHILOX) return fail(ACS_E_ARG, "unknown rng");
+    if (!(p->rho > 0.0 && p->rho < 1.0)) return fail(ACS_E_ARG, "rho (local evaporation) must be in (0,1)");
+    if (!(p->alpha > 0.0 && p->alpha < 1.0)) return fail(ACS_E_ARG, "alpha (global evaporation) must be in (0,1)");
+    if (p->q0 > 1.0) return fail(ACS_E_ARG, "q0 must be <= 1");
+    if (!(p->beta >= 0.0)) return fail(ACS_E_ARG, "beta must be >= 0");
+    const bool spm = p->variant == ACS_VARIANT_SPM || p->variant == ACS_VARIANT_SPM_SEQ;
+    if (spm && !(p->slots == 1 || p->slots == 2 || p->slots == 4 || p->slots == 8 || p->slots == 16))
+        return fail(ACS_E_ARG, "slots must be one of 1,2,4,8,16");
+    if (int rc = set_device(device)) return rc;
+
+    auto *c = new acs_gpu_ctx();
+    std::unique_ptr<acs_gpu_ctx> guard(c);
+    c->device = device;
+    c->params = *p;
+    c->n = inst->n;
+    c->m = p->ants ? p->ants : inst->n;
+    c->L = p->cl < inst->n - 1 ? p->cl : inst->n - 1;
+    c->S = spm ? p->slots : 0;
+    if (int rc = c->stream.create()) return rc;
+    cudaStream_t s = c->stream.s;
+    if (int rc = c->inst.upload(inst, true, s)) return rc;
+    const DevInstance &I = c->inst.view;
+    const uint32_t n = c->n;
+    const int bint = beta_int_of(p->beta);
+
+    // candidate lists (K2) + packed rows
+    CUDA_TRY(c->cand.alloc(static_cast<size_t>(n) * c->L));
+    CUDA_TRY(c->rows.alloc(static_cast<size_t>(n) * 32));
+    launch_topk(I, c->L, c->cand.p, s);
+    launch_build_rows(I, c->cand.p, c->L, p->beta, bint, c->rows.p, s);
+    CUDA_TRY(cudaGetLastError());
+    // tau0 = 1/(n * L_nn) from the NN tour from node 0
+    CUDA_TRY(c->best_len.alloc(1));
+    launch_nn_tour(I, 0, c->best_len.p, s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(&c->nn_len, c->best_len.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    c->tau0 = 1.0 / (static_cast<double>(n) * static_cast<double>(c->nn_len));
+    c->q0 = p->q0 < 0 ? default_q0(n) : p->q0;
+
+    if (!spm) {
+        CUDA_TRY(c->tau.alloc(static_cast<size_t>(n) * n));
+        CUDA_TRY(c->tauc.alloc(static_cast<size_t>(n) * 32));
+        launch_fill(c->tau.p, c->tau.count, c->tau0, s);
+        launch_fill(c->tauc.p, c->tauc.count, c->tau0, s);
+    } else {
+        CUDA_TRY(c->spm_ids.alloc(static_cast<size_t>(n) * c->S));
+        CUDA_TRY(c->spm_vals.alloc(static_cast<size_t>(n) * c->S));
+        CUDA_TRY(c->spm_tail.alloc(n));
+        launch_spm_init(c->spm_ids.p, c->spm_vals.p, c->spm_tail.p, n, c->S, c->tau0, s);
+    }
+    CUDA_TRY(c->routes.alloc(static_cast<size_t>(c->m) * n));
+    CUDA_TRY(c->lens.alloc(c->m));
+    CUDA_TRY(c->best_tour.alloc(n));
+    CUDA_TRY(c->iter.alloc(1));
+    CUDA_TRY(c->counters.alloc(kNumCounters));
+    CUDA_TRY(c->stats.alloc(64));
+    CUDA_TRY(cudaMemsetAsync(c->iter.p, 0, sizeof(uint64_t), s));
+    CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, c->counters.bytes(), s));
+    CUDA_TRY(cudaMemsetAsync(c->best_tour.p, 0, c->best_tour.bytes(), s));
+    const int64_t none = LLONG_MAX;
+    CUDA_TRY(cudaMemcpyAsync(c->best_len.p, &none, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+
+    if (p->variant == ACS_VARIANT_DEFERRED) {
+        CUDA_TRY(c->d_cur.alloc(c->m));
+        CUDA_TRY(c->d_start.alloc(c->m));
+        CUDA_TRY(c->d_vis.alloc(static_cast<size_t>(c->m) * I.words));
+        CUDA_TRY(c->d_rng.alloc(static_cast<size_t>(c->m) * deferred_rng_bytes(p->rng)));
+        CUDA_TRY(c->d_pend.alloc(c->m));
+        c->deferred = DevDeferred{c->d_cur.p, c->d_start.p, c->d_vis.p, c->d_rng.p, c->d_pend.p};
+    }
+
+    DevColony &C = c->colony;
+    C.m = c->m;
+    C.L = c->L;
+    C.k = p->update_period;
+    C.S = c->S;
+    C.q0 = c->q0;
+    C.beta = p->beta;
+    C.beta_int = bint;
+    C.c_l = 1.0 - p->rho;
+    C.c_0 = p->rho * c->tau0;
+    C.tau_min = c->tau0;
+    C.seed = p->seed;
+    C.rows = c->rows.p;
+    C.tau = c->tau.p;
+    C.tauc = c->tauc.p;
+    C.spm_ids = c->spm_ids.p;
+    C.spm_vals = c->spm_vals.p;
+    C.spm_tail = c->spm_tail.p;
+    C.routes = c->routes.p;
+    C.lens = c->lens.p;
+    C.counters = c->counters.p;
+    C.iter = c->iter.p;
+    DevBest &B = c->best;
+    B.tour = c->best_tour.p;
+    B.len = c->best_len.p;
+    B.alpha = p->alpha;
+    B.c_g = 1.0 - p->alpha;
+    B.iter = c->iter.p;
+    B.stats = c->stats.p;
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *out = guard.release();
+    return ACS_OK;
+}
+
+int acs_gpu_info(const acs_gpu_ctx *c, acs_ctx_info *info) {
+    if (!c || !info) return fail(ACS_E_ARG, "null ctx/info");
+    info->n = c->n;
+    info->ants = c->m;
+    info->list_len = c->L;
+    info->slots = c->S;
+    info->q0 = c->q0;
+    info->tau0 = c->tau0;
+    info->nn_len = c->nn_len;
+    info->device_bytes = c->device_bytes();
+    return ACS_OK;
+}
+
+int acs_gpu_iterate(acs_gpu_ctx *c, uint32_t n_iter, acs_iter_stats *out) {
+    if (!c) return fail(ACS_E_ARG, "null ctx");
+    if (n_iter == 0) return ACS_OK;
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->stats.count < n_iter) {
+        CUDA_TRY(c->stats.alloc(n_iter));
+        c->best.stats = c->stats.p;
+    }
+    if (int rc = c->ensure_events(2 + 2 * static_cast<size_t>(n_iter))) return rc;
+    cudaStream_t s = c->stream.s;
+    const DevInstance &I = c->inst.view;
+    const int variant = static_cast<int>(c->params.variant);
+    const int rng = static_cast<int>(c->params.rng);
+    CUDA_TRY(cudaEventRecord(c->events[0], s));
+    for (uint32_t i = 0; i < n_iter; ++i) {
+        CUDA_TRY(cudaEventRecord(c->events[2 + 2 * i], s));
+        if (variant == ACS_VARIANT_DEFERRED) {
+            launch_deferred_init(rng, I, c->colony, c->deferred, s);
+            for (uint32_t t = 1; t < c->n; ++t) {
+                launch_deferred_select(rng, I, c->colony, c->deferred, t, s);
+                if (t % c->colony.k == 0) launch_deferred_apply(I, c->colony, c->deferred, s);
+            }
+            launch_deferred_close(I, c->colony, c->deferred, s);
+        } else {
+            launch_construct(variant, rng, I, c->colony, s);
+        }
+        CUDA_TRY(cudaEventRecord(c->events[3 + 2 * i], s));
+        launch_epilogue(!c->dense(), I, c->colony, c->best, i, s);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaEventRecord(c->events[1], s));
+    if (out)
+        CUDA_TRY(cudaMemcpyAsync(out, c->stats.p, sizeof(acs_iter_stats) * n_iter,
+                                 cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    float total = 0, construct = 0;
+    CUDA_TRY(cudaEventElapsedTime(&total, c->events[0], c->events[1]));
+    for (uint32_t i = 0; i < n_iter; ++i) {
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, c->events[2 + 2 * i], c->events[3 + 2 * i]));
+        construct += ms;
+    }
+    c->last_total_ms = total;
+    c->last_construct_ms = construct;
+    return ACS_OK;
+}
+
+int acs_gpu_last_timing(const acs_gpu_ctx *c, float *total_ms, float *construct_ms) {
+    if (!c) return fail(ACS_E_ARG, "null ctx");
+    if (total_ms) *total_ms = c->last_total_ms;
+    if (construct_ms) *construct_ms = c->last_construct_ms;
+    return ACS_OK;
+}
+
+int acs_gpu_get_best(const acs_gpu_ctx *c, uint32_t *order, int64_t *len) {
+    if (!c) return fail(ACS_E_ARG, "null ctx");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream.s;
+    if (order) CUDA_TRY(cudaMemcpyAsync(order, c->best_tour.p, c->best_tour.bytes(), cudaMemcpyDeviceToHost, s));
+    if (len) CUDA_TRY(cudaMemcpyAsync(len, c->best_len.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return ACS_OK;
+}
+
+int acs_gpu_set_best(acs_gpu_ctx *c, const uint32_t *order, int64_t len) {
+    if (!c || !order) return fail(ACS_E_ARG, "null ctx/order");
+    if (len <= 0) return fail(ACS_E_ARG, "len must be > 0");
+    std::vector<uint8_t> seen(c->n, 0);
+    for (uint32_t i = 0; i < c->n; ++i) {
+        if (order[i] >= c->n || seen[order[i]]) return fail(ACS_E_ARG, "order is not a permutation");
+        seen[order[i]] = 1;
+    }
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream.s;
+    if (!c->x_tour.p) {
+        CUDA_TRY(c->x_tour.alloc(c->n));
+        CUDA_TRY(c->x_len.alloc(1));
+        CUDA_TRY(c->x_key.alloc(1));
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->x_tour.p, order, c->x_tour.bytes(), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(c->x_len.p, &len, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    launch_adopt_best(c->x_tour.p, c->x_len.p, c->inst.view, c->best, s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return ACS_OK;
+}
+
+int acs_gpu_get_routes(const acs_gpu_ctx *c, uint32_t *routes, int64_t *lengths) {
+    if (!c) return fail(ACS_E_ARG, "null ctx");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream.s;
+    if (routes) CUDA_TRY(cudaMemcpyAsync(routes, c->routes.p, c->routes.bytes(), cudaMemcpyDeviceToHost, s));
+    if (lengths) CUDA_TRY(cudaMemcpyAsync(lengths, c->lens.p, c->lens.bytes(), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return ACS_OK;
+}
+
+int acs_gpu_get_pheromone(const acs_gpu_ctx *c, double *tau) {
+    if (!c || !tau) return fail(ACS_E_ARG, "null ctx/tau");
+    if (!c->dense()) return fail(ACS_E_ARG, "selective-memory context has no dense matrix");
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMemcpyAsync(tau, c->tau.p, c->tau.bytes(), cudaMemcpyDeviceToHost, c->stream.s));
+    CUDA_TRY(cudaStreamSynchronize(c->stream.s));
+    return ACS_OK;
+}
+
+int acs_gpu_get_selective(const acs_gpu_ctx *c, uint32_t *ids, double *vals, uint32_t *tail) {
+    if (!c) return fail(ACS_E_ARG, "null ctx");
+    if (c->dense()) return fail(ACS_E_ARG, "dense context has no selective memory");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream.s;
+    if (ids) CUDA_TRY(cudaMemcpyAsync(ids, c->spm_ids.p, c->spm_ids.bytes(), cudaMemcpyDeviceToHost, s));
+    if (vals) CUDA_TRY(cudaMemcpyAsync(vals, c->spm_vals.p, c->spm_vals.bytes(), cudaMemcpyDeviceToHost, s));
+    if (tail) CUDA_TRY(cudaMemcpyAsync(tail, c->spm_tail.p, c->spm_tail.bytes(), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return ACS_OK;
+}
+
+int acs_gpu_get_candidates(const acs_gpu_ctx *c, uint32_t *flat) {
+    if (!c || !flat) return fail(ACS_E_ARG, "null ctx/flat");
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMemcpyAsync(flat, c->cand.p, c->cand.bytes(), cudaMemcpyDeviceToHost, c->stream.s));
+    CUDA_TRY(cudaStreamSynchronize(c->stream.s));
+    return ACS_OK;
+}
+
+int acs_gpu_get_counters(const acs_gpu_ctx *c, acs_counters *o) {
+    if (!c || !o) return fail(ACS_E_ARG, "null ctx/out");
+    unsigned long long h[kNumCounters];
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaMemcpyAsync(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream.s));
+    CUDA_TRY(cudaStreamSynchronize(c->stream.s));
+    o->local_updates = h[kCntUpdates];
+    o->hits = h[kCntHits];
+    o->misses = h[kCntMisses];
+    o->fallback_steps = h[kCntFallback];
+    o->greedy_steps = h[kCntGreedy];
+    o->roulette_steps = h[kCntRoulette];
+    o->cas_retries = h[kCntCasRetry];
+    o->iterations = h[kCntIters];
+    o->fallback_elems = h[kCntFallbackElems];
+    return ACS_OK;
+}
+
+void acs_gpu_destroy(acs_gpu_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream.s);
+    delete c;
+}
+
+int acs_gpu_run(const acs_instance_desc *inst, const acs_params *params, uint64_t iterations,
+                int device, uint32_t *best_order, int64_t *best_len, int64_t *trace) {
+    if (iterations == 0) return fail(ACS_E_ARG, "iterations must be > 0");
+    acs_gpu_ctx *c = nullptr;
+    if (int rc = acs_gpu_create(inst, params, device, &c)) return rc;
+    std::unique_ptr<acs_gpu_ctx, void (*)(acs_gpu_ctx *)> guard(c, acs_gpu_destroy);
+    std::vector<acs_iter_stats> st;
+    uint64_t done = 0;
+    while (done < iterations) {
+        const uint32_t chunk = static_cast<uint32_t>(std::min<uint64_t>(iterations - done, 1024));
+        st.resize(chunk);
+        if (int rc = acs_gpu_iterate(c, chunk, st.data())) return rc;
+        if (trace)
+            for (uint32_t i = 0; i < chunk; ++i) trace[done + i] = st[i].global_best_len;
+        done += chunk;
+    }
+    return acs_gpu_get_best(c, best_order, best_len);
+}
+
+// ---------------------------------------------------------------- islands
+
+int acs_gpu_nccl_unique_id(void *uid) {
+    if (!uid) return fail(ACS_E_ARG, "null unique id buffer");
+    if (int rc = g_nccl.load()) return rc;
+    nccl_uid id;
+    const int r = g_nccl.get_unique_id(&id);
+    if (r != 0) return fail(ACS_E_NCCL, std::string("ncclGetUniqueId: ") + (g_nccl.error_string ? g_nccl.error_string(r) : "?"));
+    std::memcpy(uid, &id, sizeof(id));
+    return ACS_OK;
+}
+
+int acs_gpu_island_init(acs_gpu_ctx *c, const void *uid, int nranks, int rank) {
+    if (!c || !uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(ACS_E_ARG, "bad island init args");
+    if (int rc = g_nccl.load()) return rc;
+    CUDA_TRY(cudaSetDevice(c->device));
+    nccl_uid id;
+    std::memcpy(&id, uid, sizeof(id));
+    const int r = g_nccl.comm_init_rank(&c->comm, nranks, id, rank);
+    if (r != 0) return fail(ACS_E_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.error_string ? g_nccl.error_string(r) : "?"));
+    c->rank = rank;
+    c->nranks = nranks;
+    if (!c->x_tour.p) {
+        CUDA_TRY(c->x_tour.alloc(c->n));
+        CUDA_TRY(c->x_len.alloc(1));
+        CUDA_TRY(c->x_key.alloc(1));
+    }
+    return ACS_OK;
+}
+
+}  // extern "C"
+
+extern "C" int acs_gpu_island_exchange(acs_gpu_ctx *c, int64_t *global_best_len) {
+    if (!c) return fail(ACS_E_ARG, "null ctx");
+    if (!c->comm) return fail(ACS_E_NCCL, "island not initialised (acs_gpu_island_init)");
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream.s;
+    // 1. key = L_gb << 8 | rank; min over ranks -> best colony, ties to the lowest rank
+    launch_island_pack(c->best_len.p, c->rank, c->x_key.p, s);
+    CUDA_TRY(cudaGetLastError());
+    int r = g_nccl.all_reduce(c->x_key.p, c->x_key.p, 1, kNcclInt64, kNcclMin, c->comm, s);
+    if (r != 0) return fail(ACS_E_NCCL, "ncclAllReduce(min) failed");
+    // 2. winner contributes its tour, everyone else zeros: a sum-allreduce is
+    //    a broadcast whose root is only known on the device (no host round trip)
+    launch_island_mask(c->x_key.p, c->rank, c->best_tour.p, c->n, c->x_tour.p, c->x_len.p, s);
+    CUDA_TRY(cudaGetLastError());
+    r = g_nccl.all_reduce(c->x_tour.p, c->x_tour.p, c->n, kNcclUint32, kNcclSum, c->comm, s);
+    if (r != 0) return fail(ACS_E_NCCL, "ncclAllReduce(sum) failed");
+    // 3. adopt if strictly better
+    launch_adopt_best(c->x_tour.p, c->x_len.p, c->inst.view, c->best, s);
+    CUDA_TRY(cudaGetLastError());
+    if (global_best_len) {
+        CUDA_TRY(cudaMemcpyAsync(global_best_len, c->x_len.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    return ACS_OK;
+}

@@ -1,0 +1,174 @@
+"""Tour-level parity of the sm_100a construction kernels against the CPU
+oracle (SPEC restatement).  Deterministic variants must be BIT-EXACT:
+
+  GPU ACS_VARIANT_SEQ      (k_construct_dense, one warp)  == oracle SEQ   / DENSE
+  GPU ACS_VARIANT_DEFERRED (k_def_select/apply, all ants) == oracle SYNC  / DENSE
+  GPU ACS_VARIANT_SPM_SEQ  (k_construct_spm, one warp)    == oracle SEQ   / SELECTIVE
+
+compared on: per-iteration L_gb trace, iteration-best length and ant, every
+route and length of the last iteration, the final pheromone state (dense
+matrix or selective records) and the step counters.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import assert_permutations, small_instance, to_acs
+
+pytestmark = pytest.mark.gpu
+
+GPU_OF = {("seq", O.DENSE): (O.SEQ, "seq"), ("sync", O.DENSE): (O.SYNC, "deferred"),
+          ("seq", O.SELECTIVE): (O.SEQ, "spm-seq")}
+
+
+def pair(acs, orc, I, mode, memory, *, m, iters, seed=1, k=1, beta=3.0, q0=-1.0, cl=32, s=8,
+         rng="xoshiro", alpha=0.2, rho=0.01):
+    omode, variant = GPU_OF[(mode, memory)]
+    p = acs.AcsParams(variant=variant, m=m, seed=seed, k=k, beta=beta, q0=q0, cl=cl, s=s, rng=rng,
+                      alpha=alpha, rho=rho)
+    with acs.Colony(to_acs(acs, I), p) as col:
+        st = col.iterate(iters)
+        routes, lens = col.routes()
+        state = col.pheromone() if memory == O.DENSE else col.selective()
+        cnt = col.counters()
+        best = col.best()
+    o = orc.run(I, m=m, iterations=iters, seed=seed, mode=omode, memory=memory, k=k, beta=beta,
+                q0=q0, cl=cl, s=s, rng=O.PHILOX if rng == "philox" else O.XOSHIRO, alpha=alpha,
+                rho=rho, want_tau=True, want_spm=True)
+    return st, routes, lens, state, cnt, best, o
+
+
+def check_exact(st, routes, lens, state, cnt, best, o, memory):
+    assert st["global_best_len"].tolist() == o["trace"].tolist()
+    assert st["iter_best_len"].tolist() == o["iter_best_len"].tolist()
+    assert st["iter_best_ant"].tolist() == o["iter_best_ant"].tolist()
+    assert (routes == o["routes"]).all()
+    assert lens.tolist() == o["lengths"].tolist()
+    assert best[1] == o["best_len"] and (best[0] == o["best_tour"]).all()
+    if memory == O.DENSE:
+        assert np.array_equal(state.view(np.uint64), o["tau"].view(np.uint64)), "pheromone bits differ"
+    else:
+        ids, vals, tail = state
+        assert (ids == o["spm_ids"]).all() and (tail == o["spm_tail"]).all()
+        assert np.array_equal(vals.view(np.uint64), o["spm_vals"].view(np.uint64))
+        assert cnt["hits"] == o["hits"] and cnt["misses"] == o["misses"]
+    assert cnt["fallback_steps"] == o["fallback_steps"]
+    assert cnt["greedy_steps"] == o["greedy_steps"]
+    assert cnt["roulette_steps"] == o["roulette_steps"]
+    assert cnt["local_updates"] == o["local_updates"]
+
+
+@pytest.mark.parametrize("mode,memory", [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)])
+def test_d198_bit_exact(acs, orc, gpu, mode, memory):
+    I = O.load("d198")
+    r = pair(acs, orc, I, mode, memory, m=40, iters=6)
+    check_exact(*r, memory)
+
+
+@pytest.mark.parametrize("mode,memory", [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)])
+@pytest.mark.parametrize("k", [2, 4])
+def test_update_period_bit_exact(acs, orc, gpu, mode, memory, k):
+    I = O.load("a280")
+    r = pair(acs, orc, I, mode, memory, m=24, iters=4, k=k, seed=5)
+    check_exact(*r, memory)
+
+
+@pytest.mark.parametrize("mode,memory", [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)])
+def test_philox_bit_exact(acs, orc, gpu, mode, memory):
+    I = O.load("lin318")
+    r = pair(acs, orc, I, mode, memory, m=16, iters=4, rng="philox", seed=9)
+    check_exact(*r, memory)
+
+
+@pytest.mark.parametrize("q0", [0.0, 0.5, 1.0])
+@pytest.mark.parametrize("mode", ["seq", "sync"])
+def test_q0_extremes_bit_exact(acs, orc, gpu, mode, q0):
+    # q0 = 0 -> every candidate step is a roulette draw (exercises the
+    # sequential-prefix warp roulette), q0 = 1 -> always greedy
+    I = small_instance(150, seed=4)
+    r = pair(acs, orc, I, mode, O.DENSE, m=30, iters=3, q0=q0, seed=2)
+    check_exact(*r, O.DENSE)
+
+
+@pytest.mark.parametrize("beta,cl", [(0.0, 32), (1.0, 8), (2.0, 3), (5.0, 16)])
+def test_beta_and_cl_bit_exact(acs, orc, gpu, beta, cl):
+    I = small_instance(120, seed=8)
+    for mode, memory in [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)]:
+        r = pair(acs, orc, I, mode, memory, m=20, iters=3, beta=beta, cl=cl, seed=3)
+        check_exact(*r, memory)
+
+
+@pytest.mark.parametrize("s", [1, 2, 4, 16])
+def test_spm_slots_bit_exact(acs, orc, gpu, s):
+    I = O.load("d198")
+    r = pair(acs, orc, I, "seq", O.SELECTIVE, m=20, iters=4, s=s, seed=4)
+    check_exact(*r, O.SELECTIVE)
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 31, 33])
+def test_tiny_and_ragged_instances(acs, orc, gpu, n):
+    I = small_instance(n, seed=n, scale=20)
+    for mode, memory in [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)]:
+        r = pair(acs, orc, I, mode, memory, m=7, iters=3, seed=n)
+        check_exact(*r, memory)
+
+
+def test_att_and_duplicates(acs, orc, gpu):
+    I = O.load("att532")
+    r = pair(acs, orc, I, "sync", O.DENSE, m=12, iters=2)
+    check_exact(*r, O.DENSE)
+    xs = np.array([0, 0, 3, 3, 7, 7, 7, 2, 9, 1], np.float64)  # duplicate points: d = 0 -> eps = 1 (D1)
+    ys = np.array([0, 0, 4, 4, 1, 1, 1, 8, 9, 5], np.float64)
+    I = O.Coords("dups", O.EUC_2D, xs, ys)
+    for mode, memory in [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)]:
+        check_exact(*pair(acs, orc, I, mode, memory, m=10, iters=5), memory)
+
+
+def test_sync_full_colony_pcb442(acs, orc, gpu):
+    """m = n ants in lockstep: many ants update the same edges in one step."""
+    I = O.load("pcb442")
+    r = pair(acs, orc, I, "sync", O.DENSE, m=442, iters=2, seed=17)
+    check_exact(*r, O.DENSE)
+
+
+@pytest.mark.parametrize("variant", ["atomic", "relaxed", "spm"])
+@pytest.mark.parametrize("name", ["pcb442", "rat783"])
+def test_concurrent_variants_valid(acs, orc, gpu, variant, name):
+    """Non-deterministic variants: every tour a permutation, lengths equal the
+    oracle's tour_length, L_gb monotone, update counts exact."""
+    I = O.load(name)
+    p = acs.AcsParams(variant=variant, seed=3)
+    iters = 5
+    with acs.Colony(to_acs(acs, I), p) as col:
+        st = col.iterate(iters)
+        routes, lens = col.routes()
+        cnt = col.counters()
+        best, blen = col.best()
+        if variant == "spm":
+            ids, vals, tail = col.selective()
+    assert_permutations(routes, I.n)
+    sample = range(0, I.n, 37)
+    assert [int(lens[a]) for a in sample] == [orc.tour_length(I, routes[a]) for a in sample]
+    g = st["global_best_len"]
+    assert (np.diff(g) <= 0).all() and g[-1] == blen == orc.tour_length(I, best)
+    assert st["iter_best_len"].tolist()[-1] == lens.min()
+    assert cnt["local_updates"] == iters * I.n * I.n  # k=1: n updates per tour
+    assert cnt["greedy_steps"] + cnt["roulette_steps"] + cnt["fallback_steps"] == iters * I.n * (I.n - 1)
+    if variant == "spm":  # structural invariants of the records under races
+        assert (tail < 8).all()
+        occupied = ids != 0xFFFFFFFF
+        assert (ids[occupied] < I.n).all()
+        assert np.isfinite(vals).all() and (vals > 0).all()
+        assert cnt["hits"] + cnt["misses"] == 2 * cnt["local_updates"] + 2 * I.n * iters
+
+
+def test_atomic_single_ant_equals_seq(acs, orc, gpu):
+    """With one ant there is no concurrency: the CAS variant must reproduce SEQ."""
+    I = O.load("d198")
+    p = acs.AcsParams(variant="atomic", m=1, seed=12)
+    with acs.Colony(to_acs(acs, I), p) as col:
+        st = col.iterate(8)
+        tau = col.pheromone()
+    o = orc.run(I, m=1, iterations=8, seed=12, mode=O.SEQ, want_tau=True)
+    assert st["global_best_len"].tolist() == o["trace"].tolist()
+    assert np.array_equal(tau.view(np.uint64), o["tau"].view(np.uint64))
