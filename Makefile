@@ -20,7 +20,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -warn-spill
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -ffp-contract=off -I include \
             -I /usr/local/cuda/include
 
-CU_SRCS := $(SRC)/acs_kernels.cu $(SRC)/capi.cu
+CU_SRCS := $(SRC)/k_setup.cu $(SRC)/k_colony.cu $(SRC)/capi.cu
 CXX_SRCS := $(SRC)/instance.cpp $(SRC)/solver.cpp
 CU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS))
 CXX_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CXX_SRCS))

@@ -286,6 +286,7 @@ def main():
         "roofline": roofline,
         "gpu_launches": launches_per_iter * args.steps,
         "clocks": clk.summary(),
+        "counters_per_step": {k: round((c1[k] - c0[k]) / args.steps, 1) for k in c1 if k != "iterations"},
         "quality": {"best_len": int(best_len), "optimum": opt,
                     "pct_over_opt": round(100.0 * (best_len - opt) / opt, 3) if opt else None,
                     "iterations": args.warmup + args.steps, "seeds": 1,

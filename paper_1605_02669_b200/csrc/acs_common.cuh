@@ -1,0 +1,78 @@
+// acs_common.cuh -- constants and small device helpers shared by the setup
+// (k_setup.cu) and colony (k_colony.cu) translation units.
+#pragma once
+
+#include <cstdint>
+
+#include "acs_device.cuh"
+#include "acs_kernels.cuh"
+
+namespace acs_dev {
+
+
+constexpr int kBlock = 64;            // 2 ants per CTA: fine-grained spread over 148 SMs
+constexpr int kMaxRegs = 96;          // 5 warps per SM sub-partition (16K regs each): 20 ants per SM
+constexpr int kWarpsPerBlock = kBlock / 32;
+constexpr uint32_t kIdMask = 0x00FFFFFFu;
+constexpr uint32_t kNoMirror = 0xFFu;
+
+__device__ __forceinline__ int32_t dist_of(const DevInstance &I, uint32_t u, uint32_t v,
+                                           double xu, double yu) {
+    if (I.dist) return __ldg(I.dist + static_cast<size_t>(u) * I.n + v);
+    return tsplib_distance(I.type, xu, yu, __ldg(I.xs + v), __ldg(I.ys + v));
+}
+
+__device__ __forceinline__ bool visited(const uint32_t *vis, uint32_t v) {
+    return (vis[v >> 5] >> (v & 31)) & 1u;
+}
+
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t x, int src) {
+    const uint32_t lo = __shfl_sync(kFull, static_cast<uint32_t>(x), src);
+    const uint32_t hi = __shfl_sync(kFull, static_cast<uint32_t>(x >> 32), src);
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t x, int m) {
+    const uint32_t lo = __shfl_xor_sync(kFull, static_cast<uint32_t>(x), m);
+    const uint32_t hi = __shfl_xor_sync(kFull, static_cast<uint32_t>(x >> 32), m);
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// Single-thread record update on global memory (Fig. alg:3):
+// hit -> in place, tail untouched; miss -> value from tau_min inserted at
+// (tail+1) % S evicting the least-recently inserted.  Relaxed accesses keep
+// the RELAXED contract's range invariants under races.
+__device__ __forceinline__ bool spm_update_mem(uint32_t *ids, double *vals, uint32_t *tail,
+                                               uint32_t S, uint32_t u, uint32_t v, double c_mul,
+                                               double c_add, double tau_min, double *stored) {
+    const size_t base = static_cast<size_t>(u) * S;
+    for (uint32_t j = 0; j < S; ++j) {
+        if (ld_relaxed_u32(ids + base + j) == v) {
+            const double y = affine(ld_relaxed(vals + base + j), c_mul, c_add);
+            st_relaxed(vals + base + j, y);
+            if (stored) *stored = y;
+            return true;
+        }
+    }
+    const double y = affine(tau_min, c_mul, c_add);
+    const uint32_t t = (ld_relaxed_u32(tail + u) + 1) % S;
+    st_relaxed_u32(ids + base + t, v);
+    st_relaxed(vals + base + t, y);
+    st_relaxed_u32(tail + u, t);
+    if (stored) *stored = y;
+    return false;
+}
+
+__device__ __forceinline__ double spm_read_mem(const uint32_t *ids, const double *vals, uint32_t S,
+                                               uint32_t u, uint32_t v, double tau_min) {
+    const size_t base = static_cast<size_t>(u) * S;
+    for (uint32_t j = 0; j < S; ++j)
+        if (ld_relaxed_u32(ids + base + j) == v) return ld_relaxed(vals + base + j);
+    return tau_min;
+}
+
+
+static inline unsigned blocks_for(size_t work, unsigned per) {
+    return static_cast<unsigned>((work + per - 1) / per);
+}
+
+}  // namespace acs_dev

@@ -76,9 +76,13 @@ struct Xoshiro {
         h = splitmix_next(h);
         seed(h);
     }
-    __host__ __device__ __forceinline__ uint64_t next() {
+    // the next output depends on s1 only: it can be read before the state
+    // transition is committed (speculative draws without a state copy)
+    __host__ __device__ __forceinline__ uint64_t peek() const {
         const uint64_t x = s1 * 5;
-        const uint64_t result = ((x << 7) | (x >> 57)) * 9;
+        return ((x << 7) | (x >> 57)) * 9;
+    }
+    __host__ __device__ __forceinline__ void advance() {
         const uint64_t t = s1 << 17;
         s2 ^= s0;
         s3 ^= s1;
@@ -86,6 +90,10 @@ struct Xoshiro {
         s0 ^= s3;
         s2 ^= t;
         s3 = (s3 << 45) | (s3 >> 19);
+    }
+    __host__ __device__ __forceinline__ uint64_t next() {
+        const uint64_t result = peek();
+        advance();
         return result;
     }
 };
@@ -103,7 +111,13 @@ struct Philox {
         draw = 0;
     }
     __host__ __device__ __forceinline__ uint64_t next() {
-        uint32_t c0 = draw++, c1 = ant, c2 = it_lo, c3 = it_hi, a = k0, b = k1;
+        const uint64_t r = peek();
+        advance();
+        return r;
+    }
+    __host__ __device__ __forceinline__ void advance() { ++draw; }
+    __host__ __device__ __forceinline__ uint64_t peek() const {
+        uint32_t c0 = draw, c1 = ant, c2 = it_lo, c3 = it_hi, a = k0, b = k1;
 #pragma unroll
         for (int r = 0; r < 10; ++r) {
             if (r) { a += 0x9E3779B9u; b += 0xBB67AE85u; }
@@ -198,10 +212,12 @@ __device__ __forceinline__ int warp_argmax_pos(double score, bool valid) {
     const uint32_t hi = static_cast<uint32_t>(b >> 32);
     const uint32_t lo = static_cast<uint32_t>(b);
     const uint32_t mh = __reduce_max_sync(kFull, hi);
-    const uint32_t lo2 = (valid && hi == mh) ? lo : 0u;
-    const uint32_t ml = __reduce_max_sync(kFull, lo2);
-    const unsigned win = __ballot_sync(kFull, valid && hi == mh && lo == ml);
-    return win ? __ffs(win) - 1 : -1;
+    const bool top = valid && hi == mh;
+    const unsigned th = __ballot_sync(kFull, top);
+    if ((th & (th - 1)) == 0) return th ? __ffs(th) - 1 : -1;  // unique high word: done
+    const uint32_t ml = __reduce_max_sync(kFull, top ? lo : 0u);
+    const unsigned win = __ballot_sync(kFull, top && lo == ml);
+    return __ffs(win) - 1;
 }
 
 // Roulette (Eq.2, D8, P5): sequential prefix in candidate

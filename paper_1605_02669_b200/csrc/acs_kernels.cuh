@@ -21,11 +21,13 @@ struct DevInstance {
     int type;            // acs_edge_weight
     const double *xs, *ys;
     const int32_t *dist; // n*n or nullptr (on-the-fly above 4096 nodes)
+    const double *etab;  // n*n eta^beta (fallback scan operand) or nullptr
 };
 
 struct DevColony {
     uint32_t m, L, k, S;   // ants, list length, update period, spm slots
     double q0, beta;
+    uint64_t q0_k;         // floor(q0 * 2^53): q <= q0 as a 53-bit integer compare
     int beta_int;          // >=0: integral beta (repeated multiply), -1: pow
     double c_l, c_0;       // local update tau' = c_l*tau + c_0
     double tau_min;
@@ -71,6 +73,8 @@ void launch_build_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, d
 void launch_nn_tour(const DevInstance &I, uint32_t start, int64_t *out, cudaStream_t s);
 void launch_tour_lengths(const DevInstance &I, const uint32_t *routes, uint32_t m, int64_t *out,
                          cudaStream_t s);
+void launch_eta_table(const DevInstance &I, double beta, int beta_int, double *out,
+                      cudaStream_t s);
 void launch_fill(double *p, size_t count, double value, cudaStream_t s);
 void launch_spm_init(uint32_t *ids, double *vals, uint32_t *tail, uint32_t n, uint32_t S,
                      double tau_min, cudaStream_t s);

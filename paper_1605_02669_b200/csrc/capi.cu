@@ -93,6 +93,7 @@ struct DevInst {
         view.xs = xs.p;
         view.ys = ys.p;
         view.dist = nullptr;
+        view.etab = nullptr;
         if (want_table && n <= 4096) {  // tsp_instance.hpp:31 kDistTableMaxNodes
             CUDA_TRY(dist.alloc(static_cast<size_t>(n) * n));
             launch_distance_table(view, dist.p, s);
@@ -168,7 +169,7 @@ struct acs_gpu_ctx {
     int64_t nn_len = 0;
     DBuf<uint4> rows;
     DBuf<uint32_t> cand;  // flat n*L (reference layout), kept for get_candidates
-    DBuf<double> tau, tauc, spm_vals;
+    DBuf<double> tau, tauc, spm_vals, etab;
     DBuf<uint32_t> spm_ids, spm_tail, routes, best_tour;
     DBuf<int64_t> lens, best_len;
     DBuf<uint64_t> iter;
@@ -205,7 +206,7 @@ struct acs_gpu_ctx {
         return ACS_OK;
     }
     size_t device_bytes() const {
-        return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + rows.bytes() + cand.bytes() +
+        return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + etab.bytes() + rows.bytes() + cand.bytes() +
                tau.bytes() + tauc.bytes() + spm_vals.bytes() + spm_ids.bytes() + spm_tail.bytes() +
                routes.bytes() + best_tour.bytes() + lens.bytes() + d_vis.bytes() + d_rng.bytes() +
                d_pend.bytes() + d_cur.bytes() + d_start.bytes();
@@ -419,6 +420,18 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     CUDA_TRY(cudaStreamSynchronize(s));
     c->tau0 = 1.0 / (static_cast<double>(n) * static_cast<double>(c->nn_len));
     c->q0 = p->q0 < 0 ? default_q0(n) : p->q0;
+    // The colony never reads the integer table again: the fallback scan needs
+    // eta^beta, which is tabulated instead (same n <= 4096 cut-off), and the
+    // few distances it needs come from the coordinates.
+    if (c->inst.dist.p) {
+        CUDA_TRY(c->etab.alloc(static_cast<size_t>(n) * n));
+        launch_eta_table(I, p->beta, bint, c->etab.p, s);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaStreamSynchronize(s));
+        c->inst.dist.release();
+        c->inst.view.dist = nullptr;
+        c->inst.view.etab = c->etab.p;
+    }
 
     if (!spm) {
         CUDA_TRY(c->tau.alloc(static_cast<size_t>(n) * n));
@@ -458,6 +471,7 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     C.k = p->update_period;
     C.S = c->S;
     C.q0 = c->q0;
+    C.q0_k = static_cast<uint64_t>(std::floor(c->q0 * 9007199254740992.0));  // exact: q0 * 2^53
     C.beta = p->beta;
     C.beta_int = bint;
     C.c_l = 1.0 - p->rho;

@@ -1,0 +1,894 @@
+// k_colony.cu -- per-iteration kernels of the ACS hot path (sm_100a).
+//
+//   K4 k_construct_dense   whole tour per launch, warp per ant, lane per candidate slot:
+//                          ATOMIC (CAS, CONSISTENT) / RELAXED (plain ld/st, ACS-GPU-Alt) /
+//                          SEQ (the same kernel on one warp = SPEC SEQ, bit-exact)
+//   K4 k_construct_spm     selective pheromone memory (ACS-GPU-SPM) / SPM SEQ
+//   K3 k_def_*             step-synchronous deferred variant (SPEC SYNC, bit-exact)
+//   K7 k_best              select_best (ties -> lowest ant) + strict is_better + stats
+//   K7 k_global_*          global update on the global-best edges only (D3)
+//
+// The selection loop is a dependent chain (row(cur) -> scores -> argmax -> row(v)).
+// Each step issues ONE coalesced 512 B load of the immutable packed row and ONE
+// coalesced 256 B load of candidate-ordered pheromone; the next row is prefetched
+// as soon as v is known, so the CAS of the ATOMIC variant and the bookkeeping
+// overlap the next dependent load instead of adding to it.
+#include <algorithm>
+#include <climits>
+
+#include "../../include/acs_gpu.h"
+#include "acs_common.cuh"
+
+namespace acs_dev {
+
+struct Step {
+    uint32_t v;        // chosen node
+    int pos;           // candidate position, -1 for fallback
+    uint32_t mirror;   // position of cur in v's list, kNoMirror if absent
+    double tau_old;    // trail value the selection read for (cur, v)
+    int32_t d;         // distance(cur, v)
+    int kind;          // 0 greedy, 1 roulette, 2 fallback
+};
+
+__device__ __forceinline__ unsigned long long cas64(double *p, unsigned long long expect,
+                                                    unsigned long long value) {
+    unsigned long long r;
+    asm volatile("atom.relaxed.gpu.global.cas.b64 %0, [%1], %2, %3;"
+                 : "=l"(r)
+                 : "l"(p), "l"(expect), "l"(value)
+                 : "memory");
+    return r;
+}
+
+// Predicated CAS issued by every lane without a branch: lanes with !on keep
+// got == expect.  Without divergence there is no phi at a reconvergence
+// point, so ptxas leaves the result in the ATOMG destination register and the
+// first consumer is the deferred settle loop -- the atomic round trip overlaps
+// the next row load.
+__device__ __forceinline__ unsigned long long cas64_pred(bool on, double *p,
+                                                         unsigned long long expect,
+                                                         unsigned long long value) {
+    unsigned long long got = expect;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+        "@q atom.relaxed.gpu.global.cas.b64 %0, [%1], %2, %3;\n\t}"
+        : "+l"(got)
+        : "l"(p), "l"(expect), "l"(value), "r"(static_cast<unsigned>(on))
+        : "memory");
+    return got;
+}
+
+// Full-scan fallback (Alg.2 l.18): argmax tau*eta^beta over all
+// unvisited nodes, ties -> lowest id, no RNG draw (P1).  Lane l of chunk w
+// evaluates node 32w+l, so pheromone-row and eta-row reads are coalesced
+// 256 B transactions; fully visited chunks are skipped on the (broadcast)
+// bitmask word and two chunks are in flight per iteration.
+template <class TauFn>
+__device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevColony &C,
+                                              const uint32_t *vis, uint32_t cur, TauFn tau_of,
+                                              int lane, Step &o) {
+    const double xc = __ldg(I.xs + cur), yc = __ldg(I.ys + cur);
+    const double *erow = I.etab ? I.etab + static_cast<size_t>(cur) * I.n : nullptr;
+    auto eta_of = [&](uint32_t v) -> double {
+        if (erow) return __ldg(erow + v);
+        return eta_beta(tsplib_distance(I.type, xc, yc, __ldg(I.xs + v), __ldg(I.ys + v)), C.beta,
+                        C.beta_int);
+    };
+    const uint32_t last = I.words - 1;
+    const uint32_t tail_mask = (I.n & 31) ? ((1u << (I.n & 31)) - 1u) : 0xffffffffu;
+    double bs = 0.0, bt = 0.0;
+    uint32_t bv = 0xffffffffu;
+    bool have = false;
+    constexpr int kChunks = 4;  // 4 x 32 nodes, 8 independent loads in flight per lane
+    for (uint32_t w = 0; w <= last; w += kChunks) {
+        uint32_t f[kChunks];
+        uint32_t any = 0;
+#pragma unroll
+        for (int j = 0; j < kChunks; ++j) {
+            f[j] = (w + j <= last) ? ~vis[w + j] : 0u;
+            if (w + j == last) f[j] &= tail_mask;
+            any |= f[j];
+        }
+        if (any == 0u) continue;  // warp-uniform: all visited
+        double t[kChunks], e[kChunks];
+#pragma unroll
+        for (int j = 0; j < kChunks; ++j) {
+            t[j] = 0.0;
+            e[j] = 0.0;
+            if ((f[j] >> lane) & 1u) {
+                const uint32_t v = (w + j) * 32 + lane;
+                t[j] = tau_of(v);
+                e[j] = eta_of(v);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kChunks; ++j) {
+            if ((f[j] >> lane) & 1u) {  // ascending v within the lane: strict > keeps the lowest id
+                const double s = __dmul_rn(t[j], e[j]);
+                if (!have || s > bs) { have = true; bs = s; bv = (w + j) * 32 + lane; bt = t[j]; }
+            }
+        }
+    }
+    double s = bs;
+    uint32_t node = have ? bv : 0xffffffffu;
+    warp_argmax_node(s, node, have);
+    const unsigned owner = __ballot_sync(kFull, have && bv == node);
+    o.v = node;
+    o.tau_old = __shfl_sync(kFull, bt, __ffs(owner) - 1);
+    o.d = tsplib_distance(I.type, xc, yc, __ldg(I.xs + node), __ldg(I.ys + node));
+    o.pos = -1;
+    o.kind = 2;
+    // mirror: where does cur sit in v's candidate row?
+    const uint32_t id = __ldg(&C.rows[static_cast<size_t>(node) * 32 + lane].x) & kIdMask;
+    const unsigned mm = __ballot_sync(kFull, static_cast<uint32_t>(lane) < C.L && id == cur);
+    o.mirror = mm ? static_cast<uint32_t>(__ffs(mm) - 1) : kNoMirror;
+}
+
+// The q draw of the next step, computed speculatively on a copy of the stream
+// while the next row is in flight (it does not depend on the row) and
+// committed only when that step's filtered candidate set is non-empty (P1).
+// q = (x >> 11) * 2^-53 is exact, so q <= q0  <=>  (x >> 11) <= floor(q0 * 2^53):
+// the comparison is done on the 53-bit integer (C.q0_k) without a conversion.
+// Both engines expose peek()/advance(), so no copy of the stream is needed.
+template <class RNG>
+struct Lookahead {
+    uint64_t q53;
+    __device__ __forceinline__ void prepare(const RNG &rng) {
+        q53 = rng.peek() >> 11;
+        asm volatile("" : "+l"(q53));  // keep it here: no rematerialisation on the chain
+    }
+};
+
+// Candidate branch (Eq.1 / Eq.2 over the filtered list, Alg.2 l.5-16) with the
+// P1 draw protocol; falls through to fallback_scan when all are visited.
+// Stream commit: roulette commits q (and draws r) here; for a greedy step
+// (o.kind == 0) the caller commits q with rng.advance() AFTER issuing the next
+// row load, which keeps the state transition off the dependent chain.
+template <class RNG, class TauFn>
+__device__ __forceinline__ void select_step(const DevInstance &I, const DevColony &C,
+                                            const uint32_t *vis, uint32_t cur, uint4 el,
+                                            double tau_lane, RNG &rng, const Lookahead<RNG> &la,
+                                            double *scratch, int lane, TauFn tau_of, Step &o) {
+    const uint32_t c = el.x & kIdMask;
+    const bool valid = static_cast<uint32_t>(lane) < C.L;
+    const bool unv = valid && !visited(vis, c);
+    const unsigned um = __ballot_sync(kFull, unv);
+    if (um) {
+        const double eb = __hiloint2double(static_cast<int>(el.w), static_cast<int>(el.z));
+        const double score = unv ? __dmul_rn(tau_lane, eb) : 0.0;
+        int pos;
+        if (la.q53 <= C.q0_k) {
+            pos = warp_argmax_pos(score, unv);
+            o.kind = 0;
+        } else {
+            rng.advance();  // commit q
+            const double r = uniform01(rng);
+            pos = warp_roulette_pos(score, um, r, scratch, lane);
+            o.kind = 1;
+        }
+        o.pos = pos;
+        o.v = __shfl_sync(kFull, c, pos);
+        o.mirror = __shfl_sync(kFull, el.x >> 24, pos);
+        o.d = static_cast<int32_t>(__shfl_sync(kFull, el.y, pos));
+        o.tau_old = __shfl_sync(kFull, tau_lane, pos);
+        return;
+    }
+    fallback_scan(I, C, vis, cur, tau_of, lane, o);
+}
+
+// Per-ant event counters, 32-bit (one tour has < n^2/2 fallback elements and
+// n < 2^24 steps), flushed and reset once per ant.  greedy is derived at flush
+// time as (steps - roulette - fallback).
+struct WarpCounters {
+    uint32_t fallback = 0, roulette = 0, updates = 0, retry = 0, hits = 0, misses = 0, fb_elems = 0;
+    // unvisited = n - t at step t: the elements a fallback scan touches
+    __device__ __forceinline__ void count(int kind, uint32_t unvisited) {
+        roulette += kind == 1;
+        fallback += kind == 2;
+        fb_elems += kind == 2 ? unvisited : 0u;
+    }
+    __device__ __forceinline__ void flush(unsigned long long *c, int lane, uint32_t steps) {
+        const uint32_t retries = __reduce_add_sync(kFull, retry);  // per-lane CAS retries
+        if (lane == 0) {
+            using ull = unsigned long long;
+            if (retries) atomicAdd(c + kCntCasRetry, static_cast<ull>(retries));
+            if (updates) atomicAdd(c + kCntUpdates, static_cast<ull>(updates));
+            if (hits) atomicAdd(c + kCntHits, static_cast<ull>(hits));
+            if (misses) atomicAdd(c + kCntMisses, static_cast<ull>(misses));
+            if (fallback) atomicAdd(c + kCntFallback, static_cast<ull>(fallback));
+            if (steps) atomicAdd(c + kCntGreedy, static_cast<ull>(steps - roulette - fallback));
+            if (roulette) atomicAdd(c + kCntRoulette, static_cast<ull>(roulette));
+            if (fb_elems) atomicAdd(c + kCntFallbackElems, static_cast<ull>(fb_elems));
+        }
+        fallback = roulette = updates = retry = hits = misses = fb_elems = 0;
+    }
+};
+
+// route buffered in registers: lane (t & 31) holds route[t]; one coalesced
+// 128 B store per 32 steps.
+__device__ __forceinline__ void route_put(uint32_t *route, uint32_t &rbuf, uint32_t t, uint32_t v,
+                                          int lane) {
+    if (static_cast<uint32_t>(lane) == (t & 31)) rbuf = v;
+    if ((t & 31) == 31) route[(t & ~31u) + lane] = rbuf;
+}
+__device__ __forceinline__ void route_flush(uint32_t *route, uint32_t rbuf, uint32_t last,
+                                            int lane) {
+    if ((last & 31) != 31 && static_cast<uint32_t>(lane) <= (last & 31))
+        route[(last & ~31u) + lane] = rbuf;
+}
+
+// The (up to) four copies of trail (u,v), one lane each: lane 0 tau[u][v],
+// lane 1 tau[v][u], lane 2 tauc[u][pos], lane 3 tauc[v][mirror].
+__device__ __forceinline__ double *copy_addr(const DevColony &C, uint32_t n, uint32_t u, uint32_t v,
+                                             int pos, uint32_t mirror, int lane) {
+    const bool odd = lane & 1;
+    const bool dense = lane < 2;
+    const uint32_t row = odd ? v : u;
+    const uint32_t col = dense ? (odd ? u : v) : (odd ? mirror : static_cast<uint32_t>(pos));
+    const bool ok = lane < 4 && (dense || col < 32u);
+    double *base = dense ? C.tau : C.tauc;
+    const uint32_t stride = dense ? n : 32u;
+    return ok ? base + (static_cast<size_t>(row) * stride + col) : nullptr;
+}
+
+// closing edge (last -> start): its candidate position / mirror by row search
+__device__ __forceinline__ void closing_slots(const DevColony &C, uint32_t last, uint32_t start,
+                                              int lane, int &pos, uint32_t &mirror, int32_t &d,
+                                              bool &have_d) {
+    const uint4 el = __ldg(&C.rows[static_cast<size_t>(last) * 32 + lane]);
+    const unsigned hit =
+        __ballot_sync(kFull, static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == start);
+    pos = hit ? __ffs(hit) - 1 : -1;
+    mirror = kNoMirror;
+    have_d = hit != 0;
+    d = 0;
+    if (hit) {
+        mirror = __shfl_sync(kFull, el.x >> 24, pos);
+        d = static_cast<int32_t>(__shfl_sync(kFull, el.y, pos));
+    } else {
+        const uint32_t id2 = __ldg(&C.rows[static_cast<size_t>(start) * 32 + lane].x) & kIdMask;
+        const unsigned mm = __ballot_sync(kFull, static_cast<uint32_t>(lane) < C.L && id2 == last);
+        if (mm) mirror = static_cast<uint32_t>(__ffs(mm) - 1);
+    }
+}
+
+// ============================================================ dense whole tour
+
+template <bool kAtomic, class RNG>
+__global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony C) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
+    uint32_t *vis = reinterpret_cast<uint32_t *>(smem + wpb * 32 * sizeof(double)) +
+                    static_cast<size_t>(wib) * I.words;
+    const uint64_t it = *C.iter;
+    const uint32_t n = I.n;
+    WarpCounters wc;
+
+    for (uint32_t a = blockIdx.x * wpb + wib; a < C.m; a += gridDim.x * wpb) {
+        for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
+        RNG rng;
+        rng.derive(C.seed, it, a);
+        const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));  // P1.1
+        size_t ri = static_cast<size_t>(start) * 32 + lane;
+        uint4 el = __ldg(C.rows + ri);
+        double tl = ld_relaxed(C.tauc + ri);
+        __syncwarp();
+        if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
+        __syncwarp();
+        uint32_t *route = C.routes + static_cast<size_t>(a) * n;
+        uint32_t rbuf = start, cur = start, kc = 0;
+        long long len = 0;
+        Lookahead<RNG> la;
+        la.prepare(rng);
+        // ATOMIC: per-lane in-flight CAS (lane-rotating queue, see below)
+        double *pa = nullptr;
+        unsigned long long pe = 0, pg = 0;
+        // RELAXED: the copy tauc[v][mirror] of edge (u,v) is written one step
+        // late, by the lane of row v whose candidate is u, from the value it
+        // just loaded -- row v is never written while its own load is in flight
+        // (u is visited, so the delay is invisible to this ant's selection).
+        uint32_t mprev = kEmpty;
+
+        for (uint32_t t = 1; t < n; ++t) {
+            Step st;
+            select_step(I, C, vis, cur, el, tl, rng, la, scratch, lane,
+                        [&](uint32_t v) { return ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v); },
+                        st);
+            wc.count(st.kind, n - t);
+            if constexpr (!kAtomic) {
+                if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev)
+                    st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
+                mprev = kEmpty;
+            }
+            if constexpr (kAtomic) {
+                // CONSISTENT local updates without blocking the walk: step t's
+                // four copies are CASed by lane group (t & 7); a CAS that lost
+                // to a concurrent updater is retried with the returned value,
+                // one non-blocking attempt per step, so an ant in a convoy
+                // keeps walking while its updates drain.  A lane blocks only
+                // if its group comes round again with its CAS still unresolved.
+                const bool pend = pa != nullptr;
+                const bool again = pend && pg != pe;
+                if (pend && !again) pa = nullptr;
+                wc.retry += again;
+                pe = again ? pg : pe;
+                pg = cas64_pred(again, pa, pe, dbits(affine(bitsd(pe), C.c_l, C.c_0)));
+            }
+            if (++kc == C.k) {  // D9 per-ant edge counter (warp-uniform)
+                kc = 0;
+                ++wc.updates;
+                const double nv = affine(st.tau_old, C.c_l, C.c_0);
+                if constexpr (kAtomic) {
+                    const bool mine = static_cast<uint32_t>(lane >> 2) == (t & 7);
+                    double *q = mine ? copy_addr(C, n, cur, st.v, st.pos, st.mirror, lane & 3) : nullptr;
+                    if (q && pa) {  // group slot still busy: drain it (rare)
+                        while (pg != pe) {
+                            ++wc.retry;
+                            pe = pg;
+                            pg = cas64(pa, pe, dbits(affine(bitsd(pe), C.c_l, C.c_0)));
+                        }
+                        pa = nullptr;
+                    }
+                    const bool on = q != nullptr;
+                    pe = on ? dbits(st.tau_old) : pe;
+                    pa = on ? q : pa;
+                    unsigned long long g = pg;
+                    asm volatile(
+                        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+                        "@q atom.relaxed.gpu.global.cas.b64 %0, [%1], %2, %3;\n\t}"
+                        : "+l"(g)
+                        : "l"(q), "l"(pe), "l"(dbits(nv)), "r"(static_cast<unsigned>(on))
+                        : "memory");
+                    pg = g;
+                } else {
+                    double *p = lane < 3 ? copy_addr(C, n, cur, st.v, st.pos, st.mirror, lane) : nullptr;
+                    if (p) st_relaxed(p, nv);
+                    mprev = cur;
+                }
+            }
+            // Next dependent row load.  It is issued after this step's writes:
+            // loading row v ahead of the lane-3 write to tauc[v][mirror] (same
+            // line) measured ~30% slower per step on B200 (profiles/README.md).
+            ri = static_cast<size_t>(st.v) * 32 + lane;
+            el = __ldg(C.rows + ri);
+            tl = ld_relaxed(C.tauc + ri);
+            // commit a greedy step's q draw and peek the next one, off the chain
+            if (st.kind == 0) rng.advance();
+            la.prepare(rng);
+            // every lane writes the same word: no divergent branch on the chain
+            vis[st.v >> 5] |= 1u << (st.v & 31);
+            len += st.d;
+            route_put(route, rbuf, t, st.v, lane);
+            cur = st.v;
+            __syncwarp();
+        }
+        route_flush(route, rbuf, n - 1, lane);
+        if constexpr (kAtomic) {  // drain the in-flight CAS queue
+            if (pa) {
+                while (pg != pe) {
+                    ++wc.retry;
+                    pe = pg;
+                    pg = cas64(pa, pe, dbits(affine(bitsd(pe), C.c_l, C.c_0)));
+                }
+                pa = nullptr;
+            }
+            __syncwarp();
+        } else {  // last step's deferred mirror copy (el/tl hold row `cur`)
+            if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev)
+                st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
+            __syncwarp();
+        }
+
+        // closing edge (cur -> start) is edge n of the ant (D9)
+        int pos;
+        uint32_t mirror;
+        int32_t dclose;
+        bool have_d;
+        closing_slots(C, cur, start, lane, pos, mirror, dclose, have_d);
+        if (!have_d)
+            dclose = tsplib_distance(I.type, __ldg(I.xs + cur), __ldg(I.ys + cur), __ldg(I.xs + start),
+                                     __ldg(I.ys + start));
+        if (++kc == C.k) {
+            ++wc.updates;
+            const double told = ld_relaxed(C.tau + static_cast<size_t>(cur) * n + start);
+            double *p = copy_addr(C, n, cur, start, pos, mirror, lane);
+            if (p) {
+                if constexpr (kAtomic) wc.retry += cas_affine(p, told, C.c_l, C.c_0);
+                else st_relaxed(p, affine(told, C.c_l, C.c_0));
+            }
+        }
+        if (lane == 0) C.lens[a] = len + dclose;
+        wc.flush(C.counters, lane, n - 1);
+        __syncwarp();
+    }
+}
+
+// ============================================================ selective whole tour
+
+// Register copy of one record: every lane holds all S slots (broadcast loads).
+template <int S>
+struct SpmRec {
+    uint32_t id[S];
+    double val[S];
+    uint32_t tail;
+
+    __device__ __forceinline__ void load(const DevColony &C, uint32_t u) {
+        const size_t base = static_cast<size_t>(u) * S;
+        if constexpr (S >= 4) {
+#pragma unroll
+            for (int j = 0; j < S; j += 4) {
+                const uint4 q = __ldcg(reinterpret_cast<const uint4 *>(C.spm_ids + base + j));
+                id[j] = q.x; id[j + 1] = q.y; id[j + 2] = q.z; id[j + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < S; ++j) id[j] = __ldcg(C.spm_ids + base + j);
+        }
+        if constexpr (S >= 2) {
+#pragma unroll
+            for (int j = 0; j < S; j += 2) {
+                const double2 q = __ldcg(reinterpret_cast<const double2 *>(C.spm_vals + base + j));
+                val[j] = q.x; val[j + 1] = q.y;
+            }
+        } else {
+            val[0] = __ldcg(C.spm_vals + base);
+        }
+        tail = __ldcg(C.spm_tail + u);
+    }
+    __device__ __forceinline__ double lookup(uint32_t v, double tau_min) const {
+        double r = tau_min;
+        bool found = false;
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+            if (!found && id[j] == v) { r = val[j]; found = true; }
+        return r;
+    }
+    // update record u with neighbour v; lane 0 writes through. Returns hit.
+    __device__ __forceinline__ bool update(const DevColony &C, uint32_t u, uint32_t v, double c_mul,
+                                           double c_add, int lane) {
+        int hit = -1;
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+            if (hit < 0 && id[j] == v) hit = j;
+        const size_t base = static_cast<size_t>(u) * S;
+        if (hit >= 0) {
+            double y = 0.0;
+#pragma unroll
+            for (int j = 0; j < S; ++j)
+                if (j == hit) { y = affine(val[j], c_mul, c_add); val[j] = y; }
+            if (lane == 0) st_relaxed(C.spm_vals + base + hit, y);
+            return true;
+        }
+        const double y = affine(C.tau_min, c_mul, c_add);
+        const uint32_t t = (tail + 1) % S;
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+            if (j == static_cast<int>(t)) { id[j] = v; val[j] = y; }
+        tail = t;
+        if (lane == 0) {
+            st_relaxed_u32(C.spm_ids + base + t, v);
+            st_relaxed(C.spm_vals + base + t, y);
+            st_relaxed_u32(C.spm_tail + u, t);
+        }
+        return false;
+    }
+};
+
+template <int S, class RNG>
+__global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
+    uint32_t *vis = reinterpret_cast<uint32_t *>(smem + wpb * 32 * sizeof(double)) +
+                    static_cast<size_t>(wib) * I.words;
+    const uint64_t it = *C.iter;
+    const uint32_t n = I.n;
+    WarpCounters wc;
+
+    for (uint32_t a = blockIdx.x * wpb + wib; a < C.m; a += gridDim.x * wpb) {
+        for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
+        RNG rng;
+        rng.derive(C.seed, it, a);
+        const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));
+        uint4 el = __ldg(C.rows + static_cast<size_t>(start) * 32 + lane);
+        SpmRec<S> rec;
+        rec.load(C, start);
+        __syncwarp();
+        if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
+        __syncwarp();
+        uint32_t *route = C.routes + static_cast<size_t>(a) * n;
+        uint32_t rbuf = start, cur = start, prev = 0, kc = 0;
+        bool pending = false;  // record `cur` still owes the update with `prev` (D4)
+        long long len = 0;
+        Lookahead<RNG> la;
+        la.prepare(rng);
+
+        for (uint32_t t = 1; t < n; ++t) {
+            if (pending) {
+                if (rec.update(C, cur, prev, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
+            }
+            const double tau_lane = rec.lookup(el.x & kIdMask, C.tau_min);
+            Step st;
+            select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
+                        [&](uint32_t v) { return rec.lookup(v, C.tau_min); }, st);
+            wc.count(st.kind, n - t);
+            el = __ldg(C.rows + static_cast<size_t>(st.v) * 32 + lane);  // next row first
+            pending = (++kc == C.k);
+            if (pending) {
+                kc = 0;
+                ++wc.updates;
+                if (rec.update(C, cur, st.v, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
+                prev = cur;
+            }
+            rec.load(C, st.v);  // record of the next node
+            if (st.kind == 0) rng.advance();
+            la.prepare(rng);
+            vis[st.v >> 5] |= 1u << (st.v & 31);
+            len += st.d;
+            route_put(route, rbuf, t, st.v, lane);
+            cur = st.v;
+            __syncwarp();
+        }
+        route_flush(route, rbuf, n - 1, lane);
+        if (pending) {
+            if (rec.update(C, cur, prev, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
+        }
+        const int32_t dclose = tsplib_distance(I.type, __ldg(I.xs + cur), __ldg(I.ys + cur),
+                                               __ldg(I.xs + start), __ldg(I.ys + start));
+        if (++kc == C.k) {  // closing edge: record last, then record start
+            ++wc.updates;
+            if (rec.update(C, cur, start, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
+            __syncwarp();
+            SpmRec<S> r2;
+            r2.load(C, start);
+            if (r2.update(C, start, cur, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
+        }
+        if (lane == 0) C.lens[a] = len + dclose;
+        wc.flush(C.counters, lane, n - 1);
+        __syncwarp();
+    }
+}
+
+// ============================================================ deferred (SYNC)
+
+template <class RNG>
+__global__ void k_def_init(DevInstance I, DevColony C, DevDeferred D) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (a >= C.m) return;
+    uint32_t *vis = D.vis + static_cast<size_t>(a) * I.words;
+    for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
+    RNG rng;
+    rng.derive(C.seed, *C.iter, a);
+    const uint32_t start = static_cast<uint32_t>(uniform_int(rng, I.n));
+    __syncwarp();
+    if (lane == 0) {
+        vis[start >> 5] |= 1u << (start & 31);
+        D.cur[a] = start;
+        D.start[a] = start;
+        reinterpret_cast<RNG *>(D.rng)[a] = rng;
+        C.routes[static_cast<size_t>(a) * I.n] = start;
+        C.lens[a] = 0;
+    }
+}
+
+// one step for every ant against the step-start pheromone (no writes to tau)
+template <class RNG>
+__global__ void __launch_bounds__(kBlock) k_def_select(DevInstance I, DevColony C, DevDeferred D,
+                                                       uint32_t t) {
+    __shared__ double scratch_all[kWarpsPerBlock * 32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint32_t a = blockIdx.x * kWarpsPerBlock + wib;
+    if (a >= C.m) return;
+    double *scratch = scratch_all + wib * 32;
+    uint32_t *vis = D.vis + static_cast<size_t>(a) * I.words;
+    const uint32_t cur = D.cur[a];
+    RNG rng = reinterpret_cast<RNG *>(D.rng)[a];
+    const size_t ri = static_cast<size_t>(cur) * 32 + lane;
+    const uint4 el = __ldg(C.rows + ri);
+    const double tau_lane = C.tauc[ri];
+    Step st;
+    Lookahead<RNG> la;
+    la.prepare(rng);
+    select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
+                [&](uint32_t v) { return C.tau[static_cast<size_t>(cur) * I.n + v]; }, st);
+    if (st.kind == 0) rng.advance();  // commit a greedy step's q draw
+    WarpCounters wc;
+    wc.count(st.kind, I.n - t);
+    const bool due = (t % C.k == 0);
+    if (due) ++wc.updates;
+    if (lane == 0) {
+        vis[st.v >> 5] |= 1u << (st.v & 31);
+        C.routes[static_cast<size_t>(a) * I.n + t] = st.v;
+        C.lens[a] += st.d;
+        D.cur[a] = st.v;
+        reinterpret_cast<RNG *>(D.rng)[a] = rng;
+        D.pend[a] = make_uint4(cur, st.v, (static_cast<uint32_t>(st.pos) & 0xFFu) | (st.mirror << 8),
+                               due ? 1u : 0u);
+    }
+    wc.flush(C.counters, lane, 1);
+}
+
+// apply the step's local updates: CAS on each copy (the affine maps commute,
+// so any interleaving yields f^c(tau) bit-exactly -- P7)
+__global__ void k_def_apply(DevInstance I, DevColony C, DevDeferred D) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (a >= C.m) return;
+    const uint4 p = D.pend[a];
+    if (!p.w) return;
+    const int pos = (p.z & 0xFFu) == 0xFFu ? -1 : static_cast<int>(p.z & 0xFFu);
+    double *addr = copy_addr(C, I.n, p.x, p.y, pos, (p.z >> 8) & 0xFFu, lane);
+    if (addr) cas_affine(addr, *addr, C.c_l, C.c_0);
+}
+
+// closing edges in a separate pass after step n-1 (PAPER Alg.1 l.13-14)
+__global__ void k_def_close(DevInstance I, DevColony C, DevDeferred D) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (a >= C.m) return;
+    const uint32_t last = D.cur[a], start = D.start[a];
+    int pos;
+    uint32_t mirror;
+    int32_t d;
+    bool have_d;
+    closing_slots(C, last, start, lane, pos, mirror, d, have_d);
+    if (!have_d)
+        d = tsplib_distance(I.type, __ldg(I.xs + last), __ldg(I.ys + last), __ldg(I.xs + start),
+                            __ldg(I.ys + start));
+    if (I.n % C.k == 0) {
+        double *addr = copy_addr(C, I.n, last, start, pos, mirror, lane);
+        if (addr) cas_affine(addr, *addr, C.c_l, C.c_0);
+        if (lane == 0) atomicAdd(C.counters + kCntUpdates, 1ull);
+    }
+    if (lane == 0) C.lens[a] += d;
+}
+
+// ============================================================ iteration end
+
+// select_best (ties -> lowest ant), strict is_better, best
+// tour copy, per-iteration stats; one CTA.
+__global__ void __launch_bounds__(1024) k_best(DevColony C, DevBest B, uint32_t n, uint32_t slot) {
+    __shared__ unsigned long long red_len[32];
+    __shared__ uint32_t red_ant[32];
+    __shared__ int improved;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    long long bl = LLONG_MAX;
+    uint32_t ba = 0xffffffffu;
+    for (uint32_t a = tid; a < C.m; a += blockDim.x) {
+        const long long l = C.lens[a];
+        if (l < bl) { bl = l; ba = a; }  // ascending a per thread: strict keeps lowest
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long ol = __shfl_xor_sync(kFull, bl, o);
+        const uint32_t oa = __shfl_xor_sync(kFull, ba, o);
+        if (ol < bl || (ol == bl && oa < ba)) { bl = ol; ba = oa; }
+    }
+    if (lane == 0) { red_len[wid] = static_cast<unsigned long long>(bl); red_ant[wid] = ba; }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        bl = lane < nw ? static_cast<long long>(red_len[lane]) : LLONG_MAX;
+        ba = lane < nw ? red_ant[lane] : 0xffffffffu;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long ol = __shfl_xor_sync(kFull, bl, o);
+            const uint32_t oa = __shfl_xor_sync(kFull, ba, o);
+            if (ol < bl || (ol == bl && oa < ba)) { bl = ol; ba = oa; }
+        }
+        if (lane == 0) {
+            red_len[0] = static_cast<unsigned long long>(bl);
+            red_ant[0] = ba;
+            improved = bl < *B.len;  // strict
+        }
+    }
+    __syncthreads();
+    const long long ib_len = static_cast<long long>(red_len[0]);
+    const uint32_t ib_ant = red_ant[0];
+    if (improved) {
+        const uint4 *r = reinterpret_cast<const uint4 *>(C.routes + static_cast<size_t>(ib_ant) * n);
+        if ((n & 3) == 0) {
+            for (uint32_t i = tid; i < n / 4; i += blockDim.x) reinterpret_cast<uint4 *>(B.tour)[i] = r[i];
+        } else {
+            const uint32_t *rr = C.routes + static_cast<size_t>(ib_ant) * n;
+            for (uint32_t i = tid; i < n; i += blockDim.x) B.tour[i] = rr[i];
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const long long gb = improved ? ib_len : *B.len;
+        if (improved) *B.len = ib_len;
+        acs_iter_stats *s = reinterpret_cast<acs_iter_stats *>(B.stats) + slot;
+        s->iter_best_len = ib_len;
+        s->iter_best_ant = ib_ant;
+        s->improved = improved ? 1u : 0u;
+        s->global_best_len = gb;
+        *B.iter += 1;
+        atomicAdd(C.counters + kCntIters, 1ull);
+    }
+}
+
+// dense global update, warp per global-best edge (a,b): lanes 0-3 update the
+// four copies of the trail; tour edges are distinct, so no two warps touch
+// the same word.
+__global__ void k_global_dense(DevInstance I, DevColony C, DevBest B) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t n = I.n;
+    if (i >= n) return;
+    const uint32_t a = B.tour[i], b = B.tour[i + 1 == n ? 0 : i + 1];
+    const double c_d = __dmul_rn(B.alpha, __ddiv_rn(1.0, static_cast<double>(*B.len)));
+    const uint32_t ida = __ldg(&C.rows[static_cast<size_t>(a) * 32 + lane].x);
+    const unsigned hit = __ballot_sync(kFull, static_cast<uint32_t>(lane) < C.L && (ida & kIdMask) == b);
+    const int pos = hit ? __ffs(hit) - 1 : -1;
+    uint32_t mirror = kNoMirror;
+    if (hit) {
+        mirror = __shfl_sync(kFull, ida >> 24, pos);
+    } else {
+        const uint32_t idb = __ldg(&C.rows[static_cast<size_t>(b) * 32 + lane].x) & kIdMask;
+        const unsigned mm = __ballot_sync(kFull, static_cast<uint32_t>(lane) < C.L && idb == a);
+        if (mm) mirror = static_cast<uint32_t>(__ffs(mm) - 1);
+    }
+    double *p = copy_addr(C, n, a, b, pos, mirror, lane);
+    if (p) *p = affine(*p, B.c_g, c_d);
+}
+
+// selective global update, thread per record r = tour[j]: edge j-1 (b-side,
+// neighbour tour[j-1]) precedes edge j (a-side, neighbour tour[j+1]); record
+// tour[0] goes a-side first -- exactly the sequential tour-order semantics.
+__global__ void k_global_spm(DevInstance I, DevColony C, DevBest B) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t n = I.n;
+    unsigned long long hits = 0, misses = 0;
+    if (j < n) {
+        const double c_d = __dmul_rn(B.alpha, __ddiv_rn(1.0, static_cast<double>(*B.len)));
+        const uint32_t r = B.tour[j];
+        const uint32_t nb_prev = B.tour[j == 0 ? n - 1 : j - 1];
+        const uint32_t nb_next = B.tour[j + 1 == n ? 0 : j + 1];
+        const uint32_t first = j == 0 ? nb_next : nb_prev;
+        const uint32_t second = j == 0 ? nb_prev : nb_next;
+        if (spm_update_mem(C.spm_ids, C.spm_vals, C.spm_tail, C.S, r, first, B.c_g, c_d, C.tau_min, nullptr)) ++hits; else ++misses;
+        if (spm_update_mem(C.spm_ids, C.spm_vals, C.spm_tail, C.S, r, second, B.c_g, c_d, C.tau_min, nullptr)) ++hits; else ++misses;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        hits += __shfl_xor_sync(kFull, hits, o);
+        misses += __shfl_xor_sync(kFull, misses, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (hits | misses)) {
+        atomicAdd(C.counters + kCntHits, hits);
+        atomicAdd(C.counters + kCntMisses, misses);
+    }
+}
+
+__global__ void k_adopt_best(const uint32_t *tour, const int64_t *len, uint32_t n, DevBest B) {
+    __shared__ int take;
+    if (threadIdx.x == 0) take = *len < *B.len;
+    __syncthreads();
+    if (!take) return;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) B.tour[i] = tour[i];
+    __syncthreads();
+    if (threadIdx.x == 0) *B.len = *len;
+}
+
+__global__ void k_island_pack(const int64_t *best_len, int rank, int64_t *key) {
+    *key = (*best_len << 8) | rank;
+}
+
+__global__ void k_island_mask(const int64_t *key, int rank, const uint32_t *tour, uint32_t n,
+                              uint32_t *x_tour, int64_t *x_len) {
+    const bool mine = static_cast<int>(*key & 0xFF) == rank;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        x_tour[i] = mine ? tour[i] : 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *x_len = *key >> 8;
+}
+
+// ============================================================ launchers
+
+static size_t construct_smem(const DevInstance &I, int wpb) {
+    return static_cast<size_t>(wpb) * (32 * sizeof(double) + I.words * sizeof(uint32_t));
+}
+
+template <class K>
+static void launch_tour_kernel(K kernel, const DevInstance &I, const DevColony &C, bool one_warp,
+                               cudaStream_t s) {
+    const int threads = one_warp ? 32 : kBlock;
+    const int wpb = threads / 32;
+    const unsigned grid = one_warp ? 1u : blocks_for(C.m, wpb);
+    const size_t smem = construct_smem(I, wpb);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kernel<<<grid, threads, smem, s>>>(I, C);
+}
+
+template <class RNG>
+static void launch_spm_rng(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s) {
+    switch (C.S) {
+        case 1: launch_tour_kernel(k_construct_spm<1, RNG>, I, C, one_warp, s); break;
+        case 2: launch_tour_kernel(k_construct_spm<2, RNG>, I, C, one_warp, s); break;
+        case 4: launch_tour_kernel(k_construct_spm<4, RNG>, I, C, one_warp, s); break;
+        case 8: launch_tour_kernel(k_construct_spm<8, RNG>, I, C, one_warp, s); break;
+        default: launch_tour_kernel(k_construct_spm<16, RNG>, I, C, one_warp, s); break;
+    }
+}
+
+void launch_construct(int variant, int rng, const DevInstance &I, const DevColony &C,
+                      cudaStream_t s) {
+    const bool philox = rng == ACS_RNG_PHILOX;
+    switch (variant) {
+        case ACS_VARIANT_ATOMIC:
+            if (philox) launch_tour_kernel(k_construct_dense<true, Philox>, I, C, false, s);
+            else launch_tour_kernel(k_construct_dense<true, Xoshiro>, I, C, false, s);
+            break;
+        case ACS_VARIANT_RELAXED:
+            if (philox) launch_tour_kernel(k_construct_dense<false, Philox>, I, C, false, s);
+            else launch_tour_kernel(k_construct_dense<false, Xoshiro>, I, C, false, s);
+            break;
+        case ACS_VARIANT_SEQ:
+            if (philox) launch_tour_kernel(k_construct_dense<false, Philox>, I, C, true, s);
+            else launch_tour_kernel(k_construct_dense<false, Xoshiro>, I, C, true, s);
+            break;
+        case ACS_VARIANT_SPM:
+        case ACS_VARIANT_SPM_SEQ:
+            if (philox) launch_spm_rng<Philox>(I, C, variant == ACS_VARIANT_SPM_SEQ, s);
+            else launch_spm_rng<Xoshiro>(I, C, variant == ACS_VARIANT_SPM_SEQ, s);
+            break;
+        default: break;
+    }
+}
+
+size_t deferred_rng_bytes(int rng) {
+    return rng == ACS_RNG_PHILOX ? sizeof(Philox) : sizeof(Xoshiro);
+}
+
+void launch_deferred_init(int rng, const DevInstance &I, const DevColony &C, const DevDeferred &D,
+                          cudaStream_t s) {
+    const unsigned grid = blocks_for(C.m, kWarpsPerBlock);
+    if (rng == ACS_RNG_PHILOX) k_def_init<Philox><<<grid, kBlock, 0, s>>>(I, C, D);
+    else k_def_init<Xoshiro><<<grid, kBlock, 0, s>>>(I, C, D);
+}
+
+void launch_deferred_select(int rng, const DevInstance &I, const DevColony &C,
+                            const DevDeferred &D, uint32_t step, cudaStream_t s) {
+    const unsigned grid = blocks_for(C.m, kWarpsPerBlock);
+    if (rng == ACS_RNG_PHILOX) k_def_select<Philox><<<grid, kBlock, 0, s>>>(I, C, D, step);
+    else k_def_select<Xoshiro><<<grid, kBlock, 0, s>>>(I, C, D, step);
+}
+
+void launch_deferred_apply(const DevInstance &I, const DevColony &C, const DevDeferred &D,
+                           cudaStream_t s) {
+    k_def_apply<<<blocks_for(C.m, kWarpsPerBlock), kBlock, 0, s>>>(I, C, D);
+}
+
+void launch_deferred_close(const DevInstance &I, const DevColony &C, const DevDeferred &D,
+                           cudaStream_t s) {
+    k_def_close<<<blocks_for(C.m, kWarpsPerBlock), kBlock, 0, s>>>(I, C, D);
+}
+
+void launch_epilogue(bool spm, const DevInstance &I, const DevColony &C, const DevBest &B,
+                     uint32_t slot, cudaStream_t s) {
+    k_best<<<1, 1024, 0, s>>>(C, B, I.n, slot);
+    if (spm) k_global_spm<<<blocks_for(I.n, 256), 256, 0, s>>>(I, C, B);
+    else k_global_dense<<<blocks_for(I.n, 8), 256, 0, s>>>(I, C, B);
+}
+
+void launch_adopt_best(const uint32_t *tour, const int64_t *len, const DevInstance &I,
+                       const DevBest &B, cudaStream_t s) {
+    k_adopt_best<<<1, 256, 0, s>>>(tour, len, I.n, B);
+}
+
+void launch_island_pack(const int64_t *best_len, int rank, int64_t *key, cudaStream_t s) {
+    k_island_pack<<<1, 1, 0, s>>>(best_len, rank, key);
+}
+
+void launch_island_mask(const int64_t *key, int rank, const uint32_t *best_tour, uint32_t n,
+                        uint32_t *x_tour, int64_t *x_len, cudaStream_t s) {
+    k_island_mask<<<std::min<unsigned>(blocks_for(n, 256), 64), 256, 0, s>>>(key, rank, best_tour, n,
+                                                                            x_tour, x_len);
+}
+
+}  // namespace acs_dev

@@ -1,0 +1,292 @@
+// k_setup.cu -- setup-path kernels of the ACS hot path (sm_100a):
+//   K1 k_distance_table   tsp_instance.cpp:23-47 dist_table_ (n <= 4096)
+//   K2 k_topk             tsp_instance.cpp:219-252 build_candidates (bit-exact)
+//      k_build_rows       packed candidate rows: id | mirror, distance, eta^beta
+//      k_eta_table        eta^beta of every edge (fallback scan operand, n <= 4096)
+//      k_nn_tour          tsp_instance.cpp:254-280 nn_tour_length -> tau0
+//   K6 k_tour_lengths     tsp_instance.cpp:67-78 tour_length (validation / eval)
+//   plus device RNG and selective-store op scripts used by the parity tests.
+#include <algorithm>
+#include <climits>
+
+#include "../../include/acs_gpu.h"
+#include "acs_common.cuh"
+
+namespace acs_dev {
+
+// ============================================================ setup kernels
+
+__global__ void k_distance_table(DevInstance I, int32_t *out) {
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t u = blockIdx.y;
+    if (v >= I.n) return;
+    out[static_cast<size_t>(u) * I.n + v] =
+        tsplib_distance(I.type, __ldg(I.xs + u), __ldg(I.ys + u), __ldg(I.xs + v), __ldg(I.ys + v));
+}
+
+// bitonic sort of one key per lane, ascending by lane
+__device__ __forceinline__ uint64_t warp_sort_u64(uint64_t x, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint64_t p = shfl_xor_u64(x, j);
+            const bool up = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            x = (lower == up) ? (x < p ? x : p) : (x > p ? x : p);
+        }
+    }
+    return x;
+}
+// sort a bitonic sequence ascending
+__device__ __forceinline__ uint64_t warp_merge_u64(uint64_t x, int lane) {
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint64_t p = shfl_xor_u64(x, j);
+        x = ((lane & j) == 0) ? (x < p ? x : p) : (x > p ? x : p);
+    }
+    return x;
+}
+
+// K2: warp per city keeps the 32 smallest (d<<32 | id) keys of its row as a
+// lane-sorted register list; a 32-key chunk is merged only when one of its
+// keys beats the current 32nd (ballot), so most chunks cost one distance
+// evaluation per lane.  Key order == the reference comparator (cpp:241-245).
+__global__ void __launch_bounds__(kBlock) k_topk(DevInstance I, uint32_t L, uint32_t *out) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (u >= I.n) return;
+    const double xu = __ldg(I.xs + u), yu = __ldg(I.ys + u);
+    uint64_t top = ~0ull;
+    for (uint32_t base = 0; base < I.n; base += 32) {
+        const uint32_t v = base + lane;
+        uint64_t key = ~0ull;
+        if (v < I.n && v != u) {
+            const int32_t d = tsplib_distance(I.type, xu, yu, __ldg(I.xs + v), __ldg(I.ys + v));
+            key = (static_cast<uint64_t>(static_cast<uint32_t>(d)) << 32) | v;
+        }
+        const uint64_t thr = shfl_u64(top, 31);
+        if (!__any_sync(kFull, key < thr)) continue;
+        key = warp_sort_u64(key, lane);
+        const uint64_t rev = shfl_u64(key, 31 - lane);
+        top = top < rev ? top : rev;
+        top = warp_merge_u64(top, lane);
+    }
+    if (static_cast<uint32_t>(lane) < L) out[static_cast<size_t>(u) * L + lane] = static_cast<uint32_t>(top);
+}
+
+// packed candidate rows: {id | mirror<<24, d, eta^beta lo, eta^beta hi}
+__global__ void k_build_rows(DevInstance I, const uint32_t *cand, uint32_t L, double beta,
+                             int beta_int, uint4 *rows) {
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<size_t>(I.n) * 32) return;
+    const uint32_t u = static_cast<uint32_t>(idx >> 5), p = static_cast<uint32_t>(idx & 31);
+    uint4 el = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+    if (p < L) {
+        const uint32_t c = cand[static_cast<size_t>(u) * L + p];
+        const int32_t d = tsplib_distance(I.type, I.xs[u], I.ys[u], I.xs[c], I.ys[c]);
+        const double eb = eta_beta(d, beta, beta_int);
+        uint32_t mirror = kNoMirror;
+        for (uint32_t q = 0; q < L; ++q)
+            if (cand[static_cast<size_t>(c) * L + q] == u) { mirror = q; break; }
+        const uint64_t b = dbits(eb);
+        el = make_uint4(c | (mirror << 24), static_cast<uint32_t>(d), static_cast<uint32_t>(b),
+                        static_cast<uint32_t>(b >> 32));
+    }
+    rows[idx] = el;
+}
+
+// nn_tour_length: one CTA, per step a block argmin of (d<<32 | v) over the
+// unvisited nodes (strict < in ascending v == min key), cpp:254-280.
+__global__ void __launch_bounds__(1024) k_nn_tour(DevInstance I, uint32_t start, int64_t *out) {
+    extern __shared__ uint32_t vis[];
+    __shared__ uint64_t red[32];
+    __shared__ uint64_t pick;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (uint32_t i = tid; i < I.words; i += blockDim.x) vis[i] = 0;
+    __syncthreads();
+    if (tid == 0) vis[start >> 5] |= 1u << (start & 31);
+    __syncthreads();
+    uint32_t cur = start;
+    int64_t total = 0;
+    for (uint32_t step = 1; step < I.n; ++step) {
+        const double xc = __ldg(I.xs + cur), yc = __ldg(I.ys + cur);
+        uint64_t best = ~0ull;
+        for (uint32_t v = tid; v < I.n; v += blockDim.x) {
+            if (visited(vis, v)) continue;
+            const int32_t d = dist_of(I, cur, v, xc, yc);
+            const uint64_t key = (static_cast<uint64_t>(static_cast<uint32_t>(d)) << 32) | v;
+            best = key < best ? key : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t p = shfl_xor_u64(best, o);
+            best = p < best ? p : best;
+        }
+        if (lane == 0) red[wid] = best;
+        __syncthreads();
+        if (wid == 0) {
+            uint64_t b = lane < static_cast<int>(blockDim.x >> 5) ? red[lane] : ~0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t p = shfl_xor_u64(b, o);
+                b = p < b ? p : b;
+            }
+            if (lane == 0) {
+                pick = b;
+                const uint32_t v = static_cast<uint32_t>(b);
+                vis[v >> 5] |= 1u << (v & 31);
+            }
+        }
+        __syncthreads();
+        total += static_cast<int64_t>(pick >> 32);
+        cur = static_cast<uint32_t>(pick);
+    }
+    if (tid == 0) *out = total + dist_of(I, cur, start, __ldg(I.xs + cur), __ldg(I.ys + cur));
+}
+
+// K6: warp per route, int64 closed-tour sum (cpp:67-78)
+__global__ void k_tour_lengths(DevInstance I, const uint32_t *routes, uint32_t m, int64_t *out) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (a >= m) return;
+    const uint32_t *r = routes + static_cast<size_t>(a) * I.n;
+    long long acc = 0;
+    for (uint32_t i = lane; i < I.n; i += 32) {
+        const uint32_t u = r[i == 0 ? I.n - 1 : i - 1], v = r[i];
+        acc += dist_of(I, u, v, __ldg(I.xs + u), __ldg(I.ys + u));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if (lane == 0) out[a] = acc;
+}
+
+__global__ void k_fill(double *p, size_t count, double v) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void k_spm_init(uint32_t *ids, double *vals, uint32_t *tail, uint32_t n, uint32_t S,
+                           double tau_min) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+         i < static_cast<size_t>(n) * S; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        ids[i] = kEmpty;
+        vals[i] = tau_min;
+        if (i < n) tail[i] = S - 1;  // D5: first insertion lands in slot 0
+    }
+}
+
+template <class E>
+__device__ void rng_script_body(E &e, const int32_t *ops, const uint64_t *args, uint64_t *out,
+                                uint32_t count) {
+    for (uint32_t i = 0; i < count; ++i) {
+        if (ops[i] == 0) out[i] = e.next();
+        else if (ops[i] == 1) out[i] = dbits(uniform01(e));
+        else out[i] = uniform_int(e, args[i]);
+    }
+}
+
+__global__ void k_rng_script(uint32_t kind, uint64_t seed, uint64_t it, uint64_t ant, int derive,
+                             const int32_t *ops, const uint64_t *args, uint64_t *out,
+                             uint32_t count) {
+    if (kind == ACS_RNG_PHILOX) {
+        Philox e;
+        e.derive(seed, it, ant);
+        rng_script_body(e, ops, args, out, count);
+    } else {
+        Xoshiro e;
+        if (derive) e.derive(seed, it, ant);
+        else e.seed(seed);
+        rng_script_body(e, ops, args, out, count);
+    }
+}
+
+
+__global__ void k_eta_table(DevInstance I, double beta, int beta_int, double *out) {
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t u = blockIdx.y;
+    if (v >= I.n) return;
+    const int32_t d = tsplib_distance(I.type, __ldg(I.xs + u), __ldg(I.ys + u), __ldg(I.xs + v),
+                                      __ldg(I.ys + v));
+    out[static_cast<size_t>(u) * I.n + v] = eta_beta(d, beta, beta_int);
+}
+
+__global__ void k_spm_script(uint32_t *ids, double *vals, uint32_t *tail, uint32_t S,
+                             double tau_min, double c_l, double c_0, double alpha, double c_g,
+                             const uint32_t *ops, const int64_t *lgb, uint32_t count, double *out,
+                             unsigned long long *hm) {
+    for (uint32_t i = 0; i < count; ++i) {
+        const uint32_t u = ops[3 * i], v = ops[3 * i + 1], rule = ops[3 * i + 2];
+        if (rule == 2) {
+            out[i] = spm_read_mem(ids, vals, S, u, v, tau_min);
+            continue;
+        }
+        double cm = c_l, ca = c_0;
+        if (rule == 1) {
+            cm = c_g;
+            ca = __dmul_rn(alpha, __ddiv_rn(1.0, static_cast<double>(lgb[i])));
+        }
+        const bool hit = spm_update_mem(ids, vals, tail, S, u, v, cm, ca, tau_min, &out[i]);
+        hm[hit ? 0 : 1] += 1;
+    }
+}
+
+
+// ============================================================ launchers
+
+void launch_distance_table(const DevInstance &I, int32_t *out, cudaStream_t s) {
+    dim3 grid(blocks_for(I.n, 256), I.n);
+    k_distance_table<<<grid, 256, 0, s>>>(I, out);
+}
+
+void launch_topk(const DevInstance &I, uint32_t L, uint32_t *out, cudaStream_t s) {
+    k_topk<<<blocks_for(I.n, kWarpsPerBlock), kBlock, 0, s>>>(I, L, out);
+}
+
+void launch_build_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, double beta,
+                       int beta_int, uint4 *rows, cudaStream_t s) {
+    k_build_rows<<<blocks_for(static_cast<size_t>(I.n) * 32, 256), 256, 0, s>>>(I, cand, L, beta,
+                                                                                beta_int, rows);
+}
+
+void launch_nn_tour(const DevInstance &I, uint32_t start, int64_t *out, cudaStream_t s) {
+    k_nn_tour<<<1, 1024, I.words * sizeof(uint32_t), s>>>(I, start, out);
+}
+
+void launch_tour_lengths(const DevInstance &I, const uint32_t *routes, uint32_t m, int64_t *out,
+                         cudaStream_t s) {
+    k_tour_lengths<<<blocks_for(m, 8), 256, 0, s>>>(I, routes, m, out);
+}
+
+void launch_fill(double *p, size_t count, double value, cudaStream_t s) {
+    k_fill<<<std::min<size_t>(blocks_for(count, 256), 148 * 16), 256, 0, s>>>(p, count, value);
+}
+
+void launch_spm_init(uint32_t *ids, double *vals, uint32_t *tail, uint32_t n, uint32_t S,
+                     double tau_min, cudaStream_t s) {
+    const size_t work = std::max<size_t>(static_cast<size_t>(n) * S, n);
+    k_spm_init<<<std::min<size_t>(blocks_for(work, 256), 148 * 16), 256, 0, s>>>(ids, vals, tail, n, S, tau_min);
+}
+
+void launch_rng_script(uint32_t kind, uint64_t seed, uint64_t it, uint64_t ant, int derive,
+                       const int32_t *ops, const uint64_t *args, uint64_t *out, uint32_t count,
+                       cudaStream_t s) {
+    k_rng_script<<<1, 1, 0, s>>>(kind, seed, it, ant, derive, ops, args, out, count);
+}
+
+void launch_spm_script(uint32_t *ids, double *vals, uint32_t *tail, uint32_t S, double tau_min,
+                       double c_l, double c_0, double alpha, double c_g, const uint32_t *ops,
+                       const int64_t *lgb, uint32_t count, double *out,
+                       unsigned long long *hits_misses, cudaStream_t s) {
+    k_spm_script<<<1, 1, 0, s>>>(ids, vals, tail, S, tau_min, c_l, c_0, alpha, c_g, ops, lgb,
+                                 count, out, hits_misses);
+}
+
+void launch_eta_table(const DevInstance &I, double beta, int beta_int, double *out,
+                      cudaStream_t s) {
+    dim3 grid(blocks_for(I.n, 256), I.n);
+    k_eta_table<<<grid, 256, 0, s>>>(I, beta, beta_int, out);
+}
+
+}  // namespace acs_dev
