@@ -35,6 +35,10 @@ struct DevColony {
     const uint4 *rows;     // n*32 packed candidate rows
     double *tau;           // n*n dense, or nullptr
     double *tauc;          // n*32, or nullptr
+    uint32_t *cnt;         // ATOMIC: n*n pending local updates of tau (tau = f^cnt(base))
+    uint32_t *cntc;        // ATOMIC: n*32 pending local updates of tauc
+    const double *pw_lo;   // ATOMIC: c_l^j, j < 512
+    const double *pw_hi;   // ATOMIC: c_l^(512 k), k <= m / 512
     uint32_t *spm_ids;     // n*S
     double *spm_vals;      // n*S
     uint32_t *spm_tail;    // n
@@ -101,8 +105,8 @@ void launch_deferred_close(const DevInstance &I, const DevColony &C, const DevDe
                            cudaStream_t s);
 // eval-free epilogue: iteration best (ties lowest ant), strict global best,
 // global update on the best tour, stats[slot], iter++
-void launch_epilogue(bool spm, const DevInstance &I, const DevColony &C, const DevBest &B,
-                     uint32_t slot, cudaStream_t s);
+void launch_epilogue(bool spm, bool fold, const DevInstance &I, const DevColony &C,
+                     const DevBest &B, uint32_t slot, cudaStream_t s);
 // island import: adopt (tour,len) from device buffers if strictly better
 void launch_adopt_best(const uint32_t *tour, const int64_t *len, const DevInstance &I,
                        const DevBest &B, cudaStream_t s);

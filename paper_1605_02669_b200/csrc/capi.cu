@@ -169,7 +169,8 @@ struct acs_gpu_ctx {
     int64_t nn_len = 0;
     DBuf<uint4> rows;
     DBuf<uint32_t> cand;  // flat n*L (reference layout), kept for get_candidates
-    DBuf<double> tau, tauc, spm_vals, etab;
+    DBuf<double> tau, tauc, spm_vals, etab, pw;
+    DBuf<uint32_t> cnt, cntc;  // ATOMIC variant: pending local updates per copy
     DBuf<uint32_t> spm_ids, spm_tail, routes, best_tour;
     DBuf<int64_t> lens, best_len;
     DBuf<uint64_t> iter;
@@ -438,6 +439,25 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
         CUDA_TRY(c->tauc.alloc(static_cast<size_t>(n) * 32));
         launch_fill(c->tau.p, c->tau.count, c->tau0, s);
         launch_fill(c->tauc.p, c->tauc.count, c->tau0, s);
+        if (p->variant == ACS_VARIANT_ATOMIC) {
+            CUDA_TRY(c->cnt.alloc(static_cast<size_t>(n) * n));
+            CUDA_TRY(c->cntc.alloc(static_cast<size_t>(n) * 32));
+            CUDA_TRY(cudaMemsetAsync(c->cnt.p, 0, c->cnt.bytes(), s));
+            CUDA_TRY(cudaMemsetAsync(c->cntc.p, 0, c->cntc.bytes(), s));
+            // c_l^j (j < 512) and c_l^(512k) (k <= m/512 + 1) by repeated multiplication:
+            // one copy's count per iteration is at most m (one traversal per ant)
+            const double c_l = 1.0 - p->rho;
+            const size_t hi = c->m / 512 + 2;
+            std::vector<double> pw(512 + hi);
+            pw[0] = 1.0;
+            for (size_t j = 1; j < 512; ++j) pw[j] = pw[j - 1] * c_l;
+            const double c512 = pw[511] * c_l;
+            pw[512] = 1.0;
+            for (size_t k = 1; k < hi; ++k) pw[512 + k] = pw[512 + k - 1] * c512;
+            CUDA_TRY(c->pw.alloc(pw.size()));
+            CUDA_TRY(cudaMemcpyAsync(c->pw.p, pw.data(), c->pw.bytes(), cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
     } else {
         CUDA_TRY(c->spm_ids.alloc(static_cast<size_t>(n) * c->S));
         CUDA_TRY(c->spm_vals.alloc(static_cast<size_t>(n) * c->S));
@@ -481,6 +501,10 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     C.rows = c->rows.p;
     C.tau = c->tau.p;
     C.tauc = c->tauc.p;
+    C.cnt = c->cnt.p;
+    C.cntc = c->cntc.p;
+    C.pw_lo = c->pw.p;
+    C.pw_hi = c->pw.p ? c->pw.p + 512 : nullptr;
     C.spm_ids = c->spm_ids.p;
     C.spm_vals = c->spm_vals.p;
     C.spm_tail = c->spm_tail.p;
@@ -540,7 +564,7 @@ int acs_gpu_iterate(acs_gpu_ctx *c, uint32_t n_iter, acs_iter_stats *out) {
             launch_construct(variant, rng, I, c->colony, s);
         }
         CUDA_TRY(cudaEventRecord(c->events[3 + 2 * i], s));
-        launch_epilogue(!c->dense(), I, c->colony, c->best, i, s);
+        launch_epilogue(!c->dense(), variant == ACS_VARIANT_ATOMIC, I, c->colony, c->best, i, s);
         CUDA_TRY(cudaGetLastError());
     }
     CUDA_TRY(cudaEventRecord(c->events[1], s));

@@ -30,34 +30,6 @@ struct Step {
     int kind;          // 0 greedy, 1 roulette, 2 fallback
 };
 
-__device__ __forceinline__ unsigned long long cas64(double *p, unsigned long long expect,
-                                                    unsigned long long value) {
-    unsigned long long r;
-    asm volatile("atom.relaxed.gpu.global.cas.b64 %0, [%1], %2, %3;"
-                 : "=l"(r)
-                 : "l"(p), "l"(expect), "l"(value)
-                 : "memory");
-    return r;
-}
-
-// Predicated CAS issued by every lane without a branch: lanes with !on keep
-// got == expect.  Without divergence there is no phi at a reconvergence
-// point, so ptxas leaves the result in the ATOMG destination register and the
-// first consumer is the deferred settle loop -- the atomic round trip overlaps
-// the next row load.
-__device__ __forceinline__ unsigned long long cas64_pred(bool on, double *p,
-                                                         unsigned long long expect,
-                                                         unsigned long long value) {
-    unsigned long long got = expect;
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
-        "@q atom.relaxed.gpu.global.cas.b64 %0, [%1], %2, %3;\n\t}"
-        : "+l"(got)
-        : "l"(p), "l"(expect), "l"(value), "r"(static_cast<unsigned>(on))
-        : "memory");
-    return got;
-}
-
 // Full-scan fallback (Alg.2 l.18): argmax tau*eta^beta over all
 // unvisited nodes, ties -> lowest id, no RNG draw (P1).  Lane l of chunk w
 // evaluates node 32w+l, so pheromone-row and eta-row reads are coalesced
@@ -254,8 +226,44 @@ __device__ __forceinline__ void closing_slots(const DevColony &C, uint32_t last,
 
 // ============================================================ dense whole tour
 
-template <bool kAtomic, class RNG>
+// Trail value of an ATOMIC-variant copy: base b with c pending local updates,
+// tau = f^c(b).  c <= 1 is the exact affine rule (so a lone ant -- and the
+// SEQ parity test -- is bit-identical to the CAS/sequential result); c >= 2
+// uses the closed form tau0 + c_l^c (b - tau0) with c_l^c from two small
+// power tables (lo: c & 511, hi: c >> 9).
+__device__ __forceinline__ double trail_value(double b, uint32_t c, const DevColony &C) {
+    const double one = affine(b, C.c_l, C.c_0);
+    double p = 1.0;
+    if (c >= 2u) p = __dmul_rn(__ldg(C.pw_lo + (c & 511u)), __ldg(C.pw_hi + (c >> 9)));
+    const double closed = __dadd_rn(C.tau_min, __dmul_rn(p, __dsub_rn(b, C.tau_min)));
+    return c == 0u ? b : (c == 1u ? one : closed);
+}
+
+__device__ __forceinline__ void red_add1(uint32_t *p) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+
+// index of copy `lane` (0: tau[u][v], 1: tau[v][u], 2: tauc[u][pos], 3: tauc[v][mirror])
+// into the dense (n*n) or candidate (n*32) array; returns false when absent
+__device__ __forceinline__ bool copy_index(uint32_t n, uint32_t u, uint32_t v, int pos,
+                                           uint32_t mirror, int lane, bool &dense, size_t &idx) {
+    const bool odd = lane & 1;
+    dense = lane < 2;
+    const uint32_t row = odd ? v : u;
+    const uint32_t col = dense ? (odd ? u : v) : (odd ? mirror : static_cast<uint32_t>(pos));
+    idx = static_cast<size_t>(row) * (dense ? n : 32u) + col;
+    return lane < 4 && (dense || col < 32u);
+}
+
+// kMode 0 = RELAXED (ACS-GPU-Alt): plain relaxed stores of f(tau_old), lost
+//           updates allowed; also SEQ when launched on one warp.
+// kMode 1 = ATOMIC (CONSISTENT): every local update is one contention-free
+//           `red.add` on a per-copy counter -- no update can be lost and no
+//           ant ever waits on an atomic -- and readers see f^c(base).  The
+//           iteration epilogue folds the counters back into the bases.
+template <int kMode, class RNG>
 __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony C) {
+    constexpr bool kAtomic = kMode == 1;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
@@ -274,6 +282,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
         size_t ri = static_cast<size_t>(start) * 32 + lane;
         uint4 el = __ldg(C.rows + ri);
         double tl = ld_relaxed(C.tauc + ri);
+        uint32_t cl = kAtomic ? ld_relaxed_u32(C.cntc + ri) : 0u;
         __syncwarp();
         if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
         __syncwarp();
@@ -282,9 +291,6 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
         long long len = 0;
         Lookahead<RNG> la;
         la.prepare(rng);
-        // ATOMIC: per-lane in-flight CAS (lane-rotating queue, see below)
-        double *pa = nullptr;
-        unsigned long long pe = 0, pg = 0;
         // RELAXED: the copy tauc[v][mirror] of edge (u,v) is written one step
         // late, by the lane of row v whose candidate is u, from the value it
         // just loaded -- row v is never written while its own load is in flight
@@ -293,67 +299,46 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
 
         for (uint32_t t = 1; t < n; ++t) {
             Step st;
-            select_step(I, C, vis, cur, el, tl, rng, la, scratch, lane,
-                        [&](uint32_t v) { return ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v); },
-                        st);
+            if constexpr (kAtomic) {
+                const double tv = trail_value(tl, cl, C);
+                select_step(I, C, vis, cur, el, tv, rng, la, scratch, lane,
+                            [&](uint32_t v) {
+                                const size_t k = static_cast<size_t>(cur) * n + v;
+                                return trail_value(ld_relaxed(C.tau + k), ld_relaxed_u32(C.cnt + k), C);
+                            },
+                            st);
+            } else {
+                select_step(I, C, vis, cur, el, tl, rng, la, scratch, lane,
+                            [&](uint32_t v) { return ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v); },
+                            st);
+            }
             wc.count(st.kind, n - t);
             if constexpr (!kAtomic) {
                 if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev)
                     st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
                 mprev = kEmpty;
             }
-            if constexpr (kAtomic) {
-                // CONSISTENT local updates without blocking the walk: step t's
-                // four copies are CASed by lane group (t & 7); a CAS that lost
-                // to a concurrent updater is retried with the returned value,
-                // one non-blocking attempt per step, so an ant in a convoy
-                // keeps walking while its updates drain.  A lane blocks only
-                // if its group comes round again with its CAS still unresolved.
-                const bool pend = pa != nullptr;
-                const bool again = pend && pg != pe;
-                if (pend && !again) pa = nullptr;
-                wc.retry += again;
-                pe = again ? pg : pe;
-                pg = cas64_pred(again, pa, pe, dbits(affine(bitsd(pe), C.c_l, C.c_0)));
-            }
             if (++kc == C.k) {  // D9 per-ant edge counter (warp-uniform)
                 kc = 0;
                 ++wc.updates;
-                const double nv = affine(st.tau_old, C.c_l, C.c_0);
+                bool dense;
+                size_t k;
                 if constexpr (kAtomic) {
-                    const bool mine = static_cast<uint32_t>(lane >> 2) == (t & 7);
-                    double *q = mine ? copy_addr(C, n, cur, st.v, st.pos, st.mirror, lane & 3) : nullptr;
-                    if (q && pa) {  // group slot still busy: drain it (rare)
-                        while (pg != pe) {
-                            ++wc.retry;
-                            pe = pg;
-                            pg = cas64(pa, pe, dbits(affine(bitsd(pe), C.c_l, C.c_0)));
-                        }
-                        pa = nullptr;
-                    }
-                    const bool on = q != nullptr;
-                    pe = on ? dbits(st.tau_old) : pe;
-                    pa = on ? q : pa;
-                    unsigned long long g = pg;
-                    asm volatile(
-                        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
-                        "@q atom.relaxed.gpu.global.cas.b64 %0, [%1], %2, %3;\n\t}"
-                        : "+l"(g)
-                        : "l"(q), "l"(pe), "l"(dbits(nv)), "r"(static_cast<unsigned>(on))
-                        : "memory");
-                    pg = g;
+                    if (copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k))
+                        red_add1((dense ? C.cnt : C.cntc) + k);
                 } else {
-                    double *p = lane < 3 ? copy_addr(C, n, cur, st.v, st.pos, st.mirror, lane) : nullptr;
-                    if (p) st_relaxed(p, nv);
+                    if (lane < 3 && copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k))
+                        st_relaxed((dense ? C.tau : C.tauc) + k, affine(st.tau_old, C.c_l, C.c_0));
                     mprev = cur;
                 }
             }
             // Next dependent row load.  It is issued after this step's writes:
-            // loading row v ahead of the lane-3 write to tauc[v][mirror] (same
-            // line) measured ~30% slower per step on B200 (profiles/README.md).
+            // loading row v ahead of a write to the same line measured ~30%
+            // slower per step on B200 (profiles/README.md).
             ri = static_cast<size_t>(st.v) * 32 + lane;
             el = __ldg(C.rows + ri);
             tl = ld_relaxed(C.tauc + ri);
+            if constexpr (kAtomic) cl = ld_relaxed_u32(C.cntc + ri);
             // commit a greedy step's q draw and peek the next one, off the chain
             if (st.kind == 0) rng.advance();
             la.prepare(rng);
@@ -365,21 +350,11 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
             __syncwarp();
         }
         route_flush(route, rbuf, n - 1, lane);
-        if constexpr (kAtomic) {  // drain the in-flight CAS queue
-            if (pa) {
-                while (pg != pe) {
-                    ++wc.retry;
-                    pe = pg;
-                    pg = cas64(pa, pe, dbits(affine(bitsd(pe), C.c_l, C.c_0)));
-                }
-                pa = nullptr;
-            }
-            __syncwarp();
-        } else {  // last step's deferred mirror copy (el/tl hold row `cur`)
+        if constexpr (!kAtomic) {  // last step's deferred mirror copy (el/tl hold row `cur`)
             if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev)
                 st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
-            __syncwarp();
         }
+        __syncwarp();
 
         // closing edge (cur -> start) is edge n of the ant (D9)
         int pos;
@@ -392,16 +367,41 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
                                      __ldg(I.ys + start));
         if (++kc == C.k) {
             ++wc.updates;
-            const double told = ld_relaxed(C.tau + static_cast<size_t>(cur) * n + start);
-            double *p = copy_addr(C, n, cur, start, pos, mirror, lane);
-            if (p) {
-                if constexpr (kAtomic) wc.retry += cas_affine(p, told, C.c_l, C.c_0);
-                else st_relaxed(p, affine(told, C.c_l, C.c_0));
+            bool dense;
+            size_t k;
+            if (copy_index(n, cur, start, pos, mirror, lane, dense, k)) {
+                if constexpr (kAtomic) {
+                    red_add1((dense ? C.cnt : C.cntc) + k);
+                } else {
+                    const double told = ld_relaxed(C.tau + static_cast<size_t>(cur) * n + start);
+                    st_relaxed((dense ? C.tau : C.tauc) + k, affine(told, C.c_l, C.c_0));
+                }
             }
         }
         if (lane == 0) C.lens[a] = len + dclose;
         wc.flush(C.counters, lane, n - 1);
         __syncwarp();
+    }
+}
+
+// ATOMIC variant: fold the per-copy counters into the bases (tau = f^c(base),
+// c = 0) before the global update.  Grid-stride over the dense and candidate
+// arrays; 4 counters per thread step, skipping untouched words.
+__global__ void k_fold_counts(DevColony C, size_t dense_count, size_t cand_count) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < dense_count; i += stride) {
+        const uint32_t c = C.cnt[i];
+        if (c) {
+            C.tau[i] = trail_value(C.tau[i], c, C);
+            C.cnt[i] = 0;
+        }
+    }
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cand_count; i += stride) {
+        const uint32_t c = C.cntc[i];
+        if (c) {
+            C.tauc[i] = trail_value(C.tauc[i], c, C);
+            C.cntc[i] = 0;
+        }
     }
 }
 
@@ -821,16 +821,16 @@ void launch_construct(int variant, int rng, const DevInstance &I, const DevColon
     const bool philox = rng == ACS_RNG_PHILOX;
     switch (variant) {
         case ACS_VARIANT_ATOMIC:
-            if (philox) launch_tour_kernel(k_construct_dense<true, Philox>, I, C, false, s);
-            else launch_tour_kernel(k_construct_dense<true, Xoshiro>, I, C, false, s);
+            if (philox) launch_tour_kernel(k_construct_dense<1, Philox>, I, C, false, s);
+            else launch_tour_kernel(k_construct_dense<1, Xoshiro>, I, C, false, s);
             break;
         case ACS_VARIANT_RELAXED:
-            if (philox) launch_tour_kernel(k_construct_dense<false, Philox>, I, C, false, s);
-            else launch_tour_kernel(k_construct_dense<false, Xoshiro>, I, C, false, s);
+            if (philox) launch_tour_kernel(k_construct_dense<0, Philox>, I, C, false, s);
+            else launch_tour_kernel(k_construct_dense<0, Xoshiro>, I, C, false, s);
             break;
         case ACS_VARIANT_SEQ:
-            if (philox) launch_tour_kernel(k_construct_dense<false, Philox>, I, C, true, s);
-            else launch_tour_kernel(k_construct_dense<false, Xoshiro>, I, C, true, s);
+            if (philox) launch_tour_kernel(k_construct_dense<0, Philox>, I, C, true, s);
+            else launch_tour_kernel(k_construct_dense<0, Xoshiro>, I, C, true, s);
             break;
         case ACS_VARIANT_SPM:
         case ACS_VARIANT_SPM_SEQ:
@@ -869,9 +869,12 @@ void launch_deferred_close(const DevInstance &I, const DevColony &C, const DevDe
     k_def_close<<<blocks_for(C.m, kWarpsPerBlock), kBlock, 0, s>>>(I, C, D);
 }
 
-void launch_epilogue(bool spm, const DevInstance &I, const DevColony &C, const DevBest &B,
-                     uint32_t slot, cudaStream_t s) {
+void launch_epilogue(bool spm, bool fold, const DevInstance &I, const DevColony &C,
+                     const DevBest &B, uint32_t slot, cudaStream_t s) {
     k_best<<<1, 1024, 0, s>>>(C, B, I.n, slot);
+    if (fold)
+        k_fold_counts<<<148 * 8, 256, 0, s>>>(C, static_cast<size_t>(I.n) * I.n,
+                                              static_cast<size_t>(I.n) * 32);
     if (spm) k_global_spm<<<blocks_for(I.n, 256), 256, 0, s>>>(I, C, B);
     else k_global_dense<<<blocks_for(I.n, 8), 256, 0, s>>>(I, C, B);
 }
