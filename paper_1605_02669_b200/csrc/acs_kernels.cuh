@@ -61,12 +61,11 @@ struct DevBest {
     void *stats;           // acs_iter_stats[capacity]
 };
 
-// per-ant state of the step-synchronous (deferred) variant
+// deferred variant: grid-barrier words (arrive count, generation); the per-ant
+// state lives in shared memory of the persistent kernel
 struct DevDeferred {
-    uint32_t *cur, *start;
-    uint32_t *vis;         // m * words
-    void *rng;             // m engines (Xoshiro or Philox)
-    uint4 *pend;           // m: {u, v, pos | mirror<<8, due}
+    unsigned *bar;             // [320] zero-initialised: gen, 8 group counters, root (128 B apart)
+    uint32_t ants_per_warp;    // set by the launcher
 };
 
 // ---- setup launchers (stream-ordered, async) ----
@@ -94,15 +93,10 @@ void launch_spm_script(uint32_t *ids, double *vals, uint32_t *tail, uint32_t S, 
 // variant: 0 atomic, 2 relaxed, 3 spm, 4 seq (dense, 1 warp), 5 spm seq (1 warp)
 void launch_construct(int variant, int rng, const DevInstance &I, const DevColony &C,
                       cudaStream_t s);
-// deferred (SYNC) variant: init, n-1 x (select, apply), close
-void launch_deferred_init(int rng, const DevInstance &I, const DevColony &C,
-                          const DevDeferred &D, cudaStream_t s);
-void launch_deferred_select(int rng, const DevInstance &I, const DevColony &C,
-                            const DevDeferred &D, uint32_t step, cudaStream_t s);
-void launch_deferred_apply(const DevInstance &I, const DevColony &C, const DevDeferred &D,
-                           cudaStream_t s);
-void launch_deferred_close(const DevInstance &I, const DevColony &C, const DevDeferred &D,
-                           cudaStream_t s);
+// deferred (SYNC) variant: one cooperative persistent launch per iteration;
+// returns 0, or -1 if the colony cannot be made co-resident
+int launch_deferred(int rng, const DevInstance &I, const DevColony &C, const DevDeferred &D,
+                    cudaStream_t s);
 // eval-free epilogue: iteration best (ties lowest ant), strict global best,
 // global update on the best tour, stats[slot], iter++
 void launch_epilogue(bool spm, bool fold, const DevInstance &I, const DevColony &C,
@@ -110,8 +104,6 @@ void launch_epilogue(bool spm, bool fold, const DevInstance &I, const DevColony 
 // island import: adopt (tour,len) from device buffers if strictly better
 void launch_adopt_best(const uint32_t *tour, const int64_t *len, const DevInstance &I,
                        const DevBest &B, cudaStream_t s);
-
-size_t deferred_rng_bytes(int rng);
 
 // island exchange helpers
 void launch_island_pack(const int64_t *best_len, int rank, int64_t *key, cudaStream_t s);

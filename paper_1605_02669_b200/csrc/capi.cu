@@ -176,10 +176,8 @@ struct acs_gpu_ctx {
     DBuf<uint64_t> iter;
     DBuf<unsigned long long> counters;
     DBuf<acs_iter_stats> stats;
-    // deferred variant state
-    DBuf<uint32_t> d_cur, d_start, d_vis;
-    DBuf<unsigned char> d_rng;
-    DBuf<uint4> d_pend;
+    // deferred variant: grid-barrier words
+    DBuf<unsigned> d_bar;
     // island exchange scratch
     DBuf<int64_t> x_key;
     DBuf<uint32_t> x_tour;
@@ -209,8 +207,7 @@ struct acs_gpu_ctx {
     size_t device_bytes() const {
         return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + etab.bytes() + rows.bytes() + cand.bytes() +
                tau.bytes() + tauc.bytes() + spm_vals.bytes() + spm_ids.bytes() + spm_tail.bytes() +
-               routes.bytes() + best_tour.bytes() + lens.bytes() + d_vis.bytes() + d_rng.bytes() +
-               d_pend.bytes() + d_cur.bytes() + d_start.bytes();
+               routes.bytes() + best_tour.bytes() + lens.bytes() + cnt.bytes() + cntc.bytes();
     }
 };
 
@@ -439,7 +436,7 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
         CUDA_TRY(c->tauc.alloc(static_cast<size_t>(n) * 32));
         launch_fill(c->tau.p, c->tau.count, c->tau0, s);
         launch_fill(c->tauc.p, c->tauc.count, c->tau0, s);
-        if (p->variant == ACS_VARIANT_ATOMIC) {
+        if (p->variant == ACS_VARIANT_ATOMIC || p->variant == ACS_VARIANT_DEFERRED) {
             CUDA_TRY(c->cnt.alloc(static_cast<size_t>(n) * n));
             CUDA_TRY(c->cntc.alloc(static_cast<size_t>(n) * 32));
             CUDA_TRY(cudaMemsetAsync(c->cnt.p, 0, c->cnt.bytes(), s));
@@ -477,12 +474,9 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     CUDA_TRY(cudaMemcpyAsync(c->best_len.p, &none, sizeof(int64_t), cudaMemcpyHostToDevice, s));
 
     if (p->variant == ACS_VARIANT_DEFERRED) {
-        CUDA_TRY(c->d_cur.alloc(c->m));
-        CUDA_TRY(c->d_start.alloc(c->m));
-        CUDA_TRY(c->d_vis.alloc(static_cast<size_t>(c->m) * I.words));
-        CUDA_TRY(c->d_rng.alloc(static_cast<size_t>(c->m) * deferred_rng_bytes(p->rng)));
-        CUDA_TRY(c->d_pend.alloc(c->m));
-        c->deferred = DevDeferred{c->d_cur.p, c->d_start.p, c->d_vis.p, c->d_rng.p, c->d_pend.p};
+        CUDA_TRY(c->d_bar.alloc(32 * 10));  // generation + 8 group counters + root, 128 B apart
+        CUDA_TRY(cudaMemsetAsync(c->d_bar.p, 0, c->d_bar.bytes(), s));
+        c->deferred = DevDeferred{c->d_bar.p, 1};
     }
 
     DevColony &C = c->colony;
@@ -554,12 +548,9 @@ int acs_gpu_iterate(acs_gpu_ctx *c, uint32_t n_iter, acs_iter_stats *out) {
     for (uint32_t i = 0; i < n_iter; ++i) {
         CUDA_TRY(cudaEventRecord(c->events[2 + 2 * i], s));
         if (variant == ACS_VARIANT_DEFERRED) {
-            launch_deferred_init(rng, I, c->colony, c->deferred, s);
-            for (uint32_t t = 1; t < c->n; ++t) {
-                launch_deferred_select(rng, I, c->colony, c->deferred, t, s);
-                if (t % c->colony.k == 0) launch_deferred_apply(I, c->colony, c->deferred, s);
-            }
-            launch_deferred_close(I, c->colony, c->deferred, s);
+            if (launch_deferred(rng, I, c->colony, c->deferred, s) != 0)
+                return fail(ACS_E_CUDA, std::string("deferred: cooperative launch failed (colony not co-resident): ") +
+                                            cudaGetErrorString(cudaGetLastError()));
         } else {
             launch_construct(variant, rng, I, c->colony, s);
         }

@@ -52,6 +52,7 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
     uint32_t bv = 0xffffffffu;
     bool have = false;
     constexpr int kChunks = 4;  // 4 x 32 nodes, 8 independent loads in flight per lane
+                                // (8 chunks spills at the 96-register occupancy cap)
     for (uint32_t w = 0; w <= last; w += kChunks) {
         uint32_t f[kChunks];
         uint32_t any = 0;
@@ -554,97 +555,203 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
 
 // ============================================================ deferred (SYNC)
 
+// Software grid barrier for the cooperative (all-CTAs-resident) deferred kernel:
+// one arrival per CTA on bar[0]; the last arriver resets it and bumps the
+// generation bar[1] the others spin on.
+// Two-level: CTAs arrive on one of kBarGroups group counters (own 128 B line
+// each), the last of a group arrives on the root, the last root arriver bumps
+// the generation -- 8x fewer same-address atomics on the critical arrival path.
+constexpr unsigned kBarGroups = 8;
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar;
+        const unsigned g = *gen;
+        const unsigned grp = blockIdx.x % kBarGroups;
+        const unsigned members = nblocks / kBarGroups + (grp < nblocks % kBarGroups ? 1u : 0u);
+        const unsigned groups = nblocks < kBarGroups ? nblocks : kBarGroups;
+        unsigned *gcount = bar + 32 * (1 + grp);
+        unsigned *root = bar + 32 * (1 + kBarGroups);
+        __threadfence();
+        bool release = false;
+        if (atomicAdd(gcount, 1u) == members - 1) {
+            *gcount = 0;
+            if (atomicAdd(root, 1u) == groups - 1) {
+                *root = 0;
+                release = true;
+            }
+        }
+        if (release) {
+            __threadfence();
+            atomicAdd(bar, 1u);
+        } else {
+            while (*gen == g) __nanosleep(8);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 template <class RNG>
-__global__ void k_def_init(DevInstance I, DevColony C, DevDeferred D) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (a >= C.m) return;
-    uint32_t *vis = D.vis + static_cast<size_t>(a) * I.words;
-    for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
+struct DefAnt {             // per-ant state of the deferred variant, in shared memory
     RNG rng;
-    rng.derive(C.seed, *C.iter, a);
-    const uint32_t start = static_cast<uint32_t>(uniform_int(rng, I.n));
-    __syncwarp();
-    if (lane == 0) {
-        vis[start >> 5] |= 1u << (start & 31);
-        D.cur[a] = start;
-        D.start[a] = start;
-        reinterpret_cast<RNG *>(D.rng)[a] = rng;
-        C.routes[static_cast<size_t>(a) * I.n] = start;
-        C.lens[a] = 0;
+    long long len;
+    uint32_t cur, start, v, slots;  // slots = pos | mirror << 8 of this step's edge
+};
+
+// Fold the pending count of one copy into its base by applying f c times in
+// sequence -- exactly what SYNC's ordered local updates do (P7) -- after an
+// exchange that hands the whole count to exactly one of the ants that bumped it.
+__device__ __forceinline__ void fold_copy(const DevColony &C, uint32_t n, uint32_t u, uint32_t v,
+                                          uint32_t slots, int lane) {
+    bool dense;
+    size_t k;
+    const int pos = (slots & 0xFFu) == 0xFFu ? -1 : static_cast<int>(slots & 0xFFu);
+    if (!copy_index(n, u, v, pos, (slots >> 8) & 0xFFu, lane, dense, k)) return;
+    uint32_t *cp = (dense ? C.cnt : C.cntc) + k;
+    const uint32_t c = atomicExch(cp, 0u);
+    if (c) {
+        double *bp = (dense ? C.tau : C.tauc) + k;
+        double x = ld_relaxed(bp);
+        for (uint32_t i = 0; i < c; ++i) x = affine(x, C.c_l, C.c_0);
+        st_relaxed(bp, x);
     }
 }
 
-// one step for every ant against the step-start pheromone (no writes to tau)
+__device__ __forceinline__ void bump_copy(const DevColony &C, uint32_t n, uint32_t u, uint32_t v,
+                                          uint32_t slots, int lane) {
+    bool dense;
+    size_t k;
+    const int pos = (slots & 0xFFu) == 0xFFu ? -1 : static_cast<int>(slots & 0xFFu);
+    if (copy_index(n, u, v, pos, (slots >> 8) & 0xFFu, lane, dense, k))
+        red_add1((dense ? C.cnt : C.cntc) + k);
+}
+
+// SPEC SYNC (deferred / ordered local updates) as ONE persistent cooperative
+// launch per iteration.  Per step: every ant selects against the step-start
+// pheromone and bumps the counters of its edge's copies (bases untouched);
+// grid barrier; the count of every touched copy is exchanged to one ant that
+// applies f that many times; grid barrier.  The affine updates commute, so the
+// result is bit-identical to the oracle's ant-ordered application.  Closing
+// edges are a separate pass after step n-1 (PAPER Alg.1 l.13-14).
 template <class RNG>
-__global__ void __launch_bounds__(kBlock) k_def_select(DevInstance I, DevColony C, DevDeferred D,
-                                                       uint32_t t) {
-    __shared__ double scratch_all[kWarpsPerBlock * 32];
+__global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, DevDeferred D) {
+    extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint32_t a = blockIdx.x * kWarpsPerBlock + wib;
-    if (a >= C.m) return;
-    double *scratch = scratch_all + wib * 32;
-    uint32_t *vis = D.vis + static_cast<size_t>(a) * I.words;
-    const uint32_t cur = D.cur[a];
-    RNG rng = reinterpret_cast<RNG *>(D.rng)[a];
-    const size_t ri = static_cast<size_t>(cur) * 32 + lane;
-    const uint4 el = __ldg(C.rows + ri);
-    const double tau_lane = C.tauc[ri];
-    Step st;
-    Lookahead<RNG> la;
-    la.prepare(rng);
-    select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
-                [&](uint32_t v) { return C.tau[static_cast<size_t>(cur) * I.n + v]; }, st);
-    if (st.kind == 0) rng.advance();  // commit a greedy step's q draw
+    const int wpb = blockDim.x >> 5;
+    const uint32_t A = D.ants_per_warp;
+    const uint32_t W = gridDim.x * wpb;
+    const uint32_t gw = blockIdx.x * wpb + wib;
+    const uint32_t n = I.n;
+    double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
+    DefAnt<RNG> *ants = reinterpret_cast<DefAnt<RNG> *>(smem + wpb * 32 * sizeof(double)) + wib * A;
+    uint32_t *vis_base = reinterpret_cast<uint32_t *>(smem + wpb * 32 * sizeof(double) +
+                                                      wpb * A * sizeof(DefAnt<RNG>)) +
+                         static_cast<size_t>(wib) * A * I.words;
+    const uint64_t it = *C.iter;
     WarpCounters wc;
-    wc.count(st.kind, I.n - t);
-    const bool due = (t % C.k == 0);
-    if (due) ++wc.updates;
-    if (lane == 0) {
-        vis[st.v >> 5] |= 1u << (st.v & 31);
-        C.routes[static_cast<size_t>(a) * I.n + t] = st.v;
-        C.lens[a] += st.d;
-        D.cur[a] = st.v;
-        reinterpret_cast<RNG *>(D.rng)[a] = rng;
-        D.pend[a] = make_uint4(cur, st.v, (static_cast<uint32_t>(st.pos) & 0xFFu) | (st.mirror << 8),
-                               due ? 1u : 0u);
-    }
-    wc.flush(C.counters, lane, 1);
-}
+    uint32_t my_ants = 0;
 
-// apply the step's local updates: CAS on each copy (the affine maps commute,
-// so any interleaving yields f^c(tau) bit-exactly -- P7)
-__global__ void k_def_apply(DevInstance I, DevColony C, DevDeferred D) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (a >= C.m) return;
-    const uint4 p = D.pend[a];
-    if (!p.w) return;
-    const int pos = (p.z & 0xFFu) == 0xFFu ? -1 : static_cast<int>(p.z & 0xFFu);
-    double *addr = copy_addr(C, I.n, p.x, p.y, pos, (p.z >> 8) & 0xFFu, lane);
-    if (addr) cas_affine(addr, *addr, C.c_l, C.c_0);
-}
-
-// closing edges in a separate pass after step n-1 (PAPER Alg.1 l.13-14)
-__global__ void k_def_close(DevInstance I, DevColony C, DevDeferred D) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (a >= C.m) return;
-    const uint32_t last = D.cur[a], start = D.start[a];
-    int pos;
-    uint32_t mirror;
-    int32_t d;
-    bool have_d;
-    closing_slots(C, last, start, lane, pos, mirror, d, have_d);
-    if (!have_d)
-        d = tsplib_distance(I.type, __ldg(I.xs + last), __ldg(I.ys + last), __ldg(I.xs + start),
-                            __ldg(I.ys + start));
-    if (I.n % C.k == 0) {
-        double *addr = copy_addr(C, I.n, last, start, pos, mirror, lane);
-        if (addr) cas_affine(addr, *addr, C.c_l, C.c_0);
-        if (lane == 0) atomicAdd(C.counters + kCntUpdates, 1ull);
+    for (uint32_t j = 0; j < A; ++j) {
+        const uint32_t a = gw + j * W;
+        if (a >= C.m) break;
+        ++my_ants;
+        uint32_t *vis = vis_base + j * I.words;
+        for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
+        RNG rng;
+        rng.derive(C.seed, it, a);
+        const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));
+        __syncwarp();
+        if (lane == 0) {
+            vis[start >> 5] |= 1u << (start & 31);
+            ants[j].rng = rng;
+            ants[j].len = 0;
+            ants[j].cur = start;
+            ants[j].start = start;
+            C.routes[static_cast<size_t>(a) * n] = start;
+        }
+        __syncwarp();
     }
-    if (lane == 0) C.lens[a] += d;
+    grid_sync(D.bar, gridDim.x);
+
+    for (uint32_t t = 1; t < n; ++t) {
+        const bool due = (t % C.k) == 0;
+        for (uint32_t j = 0; j < my_ants; ++j) {
+            const uint32_t a = gw + j * W;
+            uint32_t *vis = vis_base + j * I.words;
+            DefAnt<RNG> &s = ants[j];
+            const uint32_t cur = s.cur;
+            RNG rng = s.rng;
+            const size_t ri = static_cast<size_t>(cur) * 32 + lane;
+            const uint4 el = __ldg(C.rows + ri);
+            const double tau_lane = ld_relaxed(C.tauc + ri);
+            Lookahead<RNG> la;
+            la.prepare(rng);
+            Step st;
+            select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
+                        [&](uint32_t v) { return ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v); },
+                        st);
+            if (st.kind == 0) rng.advance();
+            wc.count(st.kind, n - t);
+            const uint32_t slots = (static_cast<uint32_t>(st.pos) & 0xFFu) | (st.mirror << 8);
+            if (due) {
+                ++wc.updates;
+                bump_copy(C, n, cur, st.v, slots, lane);
+            }
+            vis[st.v >> 5] |= 1u << (st.v & 31);
+            __syncwarp();
+            if (lane == 0) {
+                C.routes[static_cast<size_t>(a) * n + t] = st.v;
+                s.rng = rng;
+                s.len += st.d;
+                s.v = st.v;
+                s.slots = slots;
+            }
+            __syncwarp();
+        }
+        grid_sync(D.bar, gridDim.x);
+        for (uint32_t j = 0; j < my_ants; ++j) {
+            DefAnt<RNG> &s = ants[j];
+            if (due) fold_copy(C, n, s.cur, s.v, s.slots, lane);
+            __syncwarp();
+            if (lane == 0) s.cur = s.v;
+            __syncwarp();
+        }
+        if (due) grid_sync(D.bar, gridDim.x);
+    }
+
+    // closing edges: a separate pass after step n-1
+    const bool close_due = (n % C.k) == 0;
+    uint32_t close_slots[1] = {0};
+    for (uint32_t j = 0; j < my_ants; ++j) {
+        const uint32_t a = gw + j * W;
+        DefAnt<RNG> &s = ants[j];
+        int pos;
+        uint32_t mirror;
+        int32_t d;
+        bool have_d;
+        closing_slots(C, s.cur, s.start, lane, pos, mirror, d, have_d);
+        if (!have_d)
+            d = tsplib_distance(I.type, __ldg(I.xs + s.cur), __ldg(I.ys + s.cur), __ldg(I.xs + s.start),
+                                __ldg(I.ys + s.start));
+        const uint32_t slots = (static_cast<uint32_t>(pos) & 0xFFu) | (mirror << 8);
+        if (close_due) {
+            ++wc.updates;
+            bump_copy(C, n, s.cur, s.start, slots, lane);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            C.lens[a] = s.len + d;
+            s.slots = slots;
+        }
+        __syncwarp();
+    }
+    (void)close_slots;
+    if (close_due) {
+        grid_sync(D.bar, gridDim.x);
+        for (uint32_t j = 0; j < my_ants; ++j) fold_copy(C, n, ants[j].cur, ants[j].start, ants[j].slots, lane);
+    }
+    wc.flush(C.counters, lane, my_ants * (n - 1));
 }
 
 // ============================================================ iteration end
@@ -841,32 +948,36 @@ void launch_construct(int variant, int rng, const DevInstance &I, const DevColon
     }
 }
 
-size_t deferred_rng_bytes(int rng) {
-    return rng == ACS_RNG_PHILOX ? sizeof(Philox) : sizeof(Xoshiro);
+template <class RNG>
+static int deferred_launch(const DevInstance &I, const DevColony &C, DevDeferred D, cudaStream_t s) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int wpb = kDefBlock / 32;
+    auto smem_for = [&](uint32_t A) {
+        return static_cast<size_t>(wpb) * (32 * sizeof(double) + A * sizeof(DefAnt<RNG>) +
+                                           static_cast<size_t>(A) * I.words * sizeof(uint32_t));
+    };
+    uint32_t A = 1;
+    size_t smem = 0;
+    for (;; ++A) {
+        smem = smem_for(A);
+        if (smem > 200 * 1024) return -1;
+        cudaFuncSetAttribute(k_deferred<RNG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_deferred<RNG>, kDefBlock, smem);
+        if (per_sm < 1) return -1;
+        if (static_cast<uint64_t>(sms) * per_sm * wpb * A >= C.m) break;
+    }
+    const unsigned grid = std::min<unsigned>(sms * per_sm, blocks_for(blocks_for(C.m, A), wpb));
+    D.ants_per_warp = A;
+    void *args[] = {const_cast<DevInstance *>(&I), const_cast<DevColony *>(&C), &D};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void *>(k_deferred<RNG>), grid, kDefBlock, args,
+                                       smem, s) == cudaSuccess ? 0 : -1;
 }
 
-void launch_deferred_init(int rng, const DevInstance &I, const DevColony &C, const DevDeferred &D,
-                          cudaStream_t s) {
-    const unsigned grid = blocks_for(C.m, kWarpsPerBlock);
-    if (rng == ACS_RNG_PHILOX) k_def_init<Philox><<<grid, kBlock, 0, s>>>(I, C, D);
-    else k_def_init<Xoshiro><<<grid, kBlock, 0, s>>>(I, C, D);
-}
-
-void launch_deferred_select(int rng, const DevInstance &I, const DevColony &C,
-                            const DevDeferred &D, uint32_t step, cudaStream_t s) {
-    const unsigned grid = blocks_for(C.m, kWarpsPerBlock);
-    if (rng == ACS_RNG_PHILOX) k_def_select<Philox><<<grid, kBlock, 0, s>>>(I, C, D, step);
-    else k_def_select<Xoshiro><<<grid, kBlock, 0, s>>>(I, C, D, step);
-}
-
-void launch_deferred_apply(const DevInstance &I, const DevColony &C, const DevDeferred &D,
-                           cudaStream_t s) {
-    k_def_apply<<<blocks_for(C.m, kWarpsPerBlock), kBlock, 0, s>>>(I, C, D);
-}
-
-void launch_deferred_close(const DevInstance &I, const DevColony &C, const DevDeferred &D,
-                           cudaStream_t s) {
-    k_def_close<<<blocks_for(C.m, kWarpsPerBlock), kBlock, 0, s>>>(I, C, D);
+int launch_deferred(int rng, const DevInstance &I, const DevColony &C, const DevDeferred &D,
+                    cudaStream_t s) {
+    return rng == ACS_RNG_PHILOX ? deferred_launch<Philox>(I, C, D, s) : deferred_launch<Xoshiro>(I, C, D, s);
 }
 
 void launch_epilogue(bool spm, bool fold, const DevInstance &I, const DevColony &C,
