@@ -34,7 +34,7 @@ PAPER_ACS_GPU_PR2392 = 4942.0  # ACS-GPU (atomic) pr2392, GK104, PA
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--instance", default="pr2392")
@@ -45,6 +45,7 @@ def parse_args():
     ap.add_argument("--exchange-every", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     return ap.parse_args()
 
 
@@ -158,29 +159,32 @@ def run_reference(args):
     memory = O.SELECTIVE if args.variant in ("spm", "spm-seq") else O.DENSE
     consistent = 1 if args.variant == "atomic" else 0
     orc = O.Oracle()
-    # warmup + timed steps, one iteration each (the oracle keeps no state across calls,
-    # so each step is a fresh single-iteration colony: same per-iteration work)
-    for _ in range(args.warmup):
-        orc.run(I, m=m, iterations=1, seed=args.seed, mode=mode, memory=memory, consistent=consistent,
-                threads=threads, k=args.k, want_routes=False)
+    # Each step is one ACS iteration of a bounded sample of the colony
+    # (min(m, 1024) ants) so that --steps K --warmup W stays within minutes;
+    # the metric is per tour, so the sample does not bias it.  The oracle keeps
+    # no state across calls: every step is a fresh single-iteration colony.
+    m_step = min(m, 1024)
+    for w in range(args.warmup):
+        orc.run(I, m=m_step, iterations=1, seed=args.seed + 1000 + w, mode=mode, memory=memory,
+                consistent=consistent, threads=threads, k=args.k, want_routes=False)
     loop_ms = []
-    for s in range(args.steps):
-        o = orc.run(I, m=m, iterations=1, seed=args.seed + s, mode=mode, memory=memory,
+    for st in range(args.steps):
+        o = orc.run(I, m=m_step, iterations=1, seed=args.seed + st, mode=mode, memory=memory,
                     consistent=consistent, threads=threads, k=args.k, want_routes=False)
         loop_ms.append(o["loop_ms"])
     total_s = sum(loop_ms) / 1e3
-    value = m * args.steps / total_s
+    value = m_step * args.steps / total_s
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "tours/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(sum(loop_ms) / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(sum(loop_ms) / args.steps * m / m_step, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": f"TSPLIB {args.instance} (real instance)",
         "config": {"workload": f"{args.instance} ACS, {m} ants, cl=32, k={args.k}, {args.variant}",
                    "variant": args.variant, "mode": ["seq", "sync", "relaxed"][mode],
                    "memory": ["dense", "selective"][memory], "consistent": consistent},
         "cpu_baseline": {"value": round(value, 1), "unit": "tours/s", "cores": threads, "kind": "port",
                          "sample": f"oracle/acs_oracle.c OpenMP on {threads} host threads, "
-                                   f"{args.steps} iterations x {m} tours"},
+                                   f"{args.steps} iterations x {m_step} of {m} ants per step"},
         "e2e": {"value": round(value, 1), "unit": "tours/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -218,7 +222,9 @@ def main():
         col.island_init(uid[0], world, rank)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
-    launches_per_iter = 2 if args.variant != "deferred" else 3 + (inst.n - 1) + (inst.n - 1) // args.k
+    # our kernels per iteration: construction (1 launch; deferred = 1 cooperative
+    # launch) + k_best + global update (+ k_fold_counts for atomic)
+    launches_per_iter = 3 + (1 if args.variant == "atomic" else 0)
 
     def step(i):
         flush.fill_(i & 0xFF)  # evict L2 (126 MB) before the step
@@ -292,6 +298,8 @@ def main():
                     "iterations": args.warmup + args.steps, "seeds": 1,
                     "note": "single run; 30-seed study in profiles/quality_*.json"},
     }
+    if rank == 0 and not args.no_variants:
+        line["variants"] = other_variants(P, inst, args, local)
     if rank == 0 and not args.no_e2e:
         line["e2e"] = e2e(P, inst, params, args, world)
     if rank == 0 and not args.no_cpu_baseline:
@@ -302,6 +310,29 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def other_variants(P, inst, args, device):
+    """Secondary numbers: the other pheromone memories on the same workload
+    (same flush + per-step event timing, 5 steps each)."""
+    import torch
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
+    out = {}
+    for v in ("atomic", "relaxed", "spm", "deferred"):
+        if v == args.variant:
+            continue
+        p = P.AcsParams(variant=v, m=args.ants or inst.n, k=args.k, seed=args.seed)
+        with P.Colony(inst, p, device=device) as col:
+            col.iterate(2)
+            ms = []
+            for i in range(5):
+                flush.fill_(i)
+                torch.cuda.synchronize()
+                col.iterate(1)
+                ms.append(col.last_timing()[0])
+        t = sum(ms) / len(ms)
+        out[v] = {"ms_per_step": round(t, 4), "tours_per_s": round(col.m / (t / 1e3), 1)}
+    return out
 
 
 def e2e(P, inst, params, args, world):

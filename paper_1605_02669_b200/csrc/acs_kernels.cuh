@@ -38,7 +38,8 @@ struct DevColony {
     uint32_t *cnt;         // ATOMIC: n*n pending local updates of tau (tau = f^cnt(base))
     uint32_t *cntc;        // ATOMIC: n*32 pending local updates of tauc
     const double *pw_lo;   // ATOMIC: c_l^j, j < 512
-    const double *pw_hi;   // ATOMIC: c_l^(512 k), k <= m / 512
+    const double *pw_hi;   // ATOMIC: c_l^(512 k), k < pw_hi_n
+    uint32_t pw_hi_n;
     uint32_t *spm_ids;     // n*S
     double *spm_vals;      // n*S
     uint32_t *spm_tail;    // n

@@ -499,6 +499,7 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     C.cntc = c->cntc.p;
     C.pw_lo = c->pw.p;
     C.pw_hi = c->pw.p ? c->pw.p + 512 : nullptr;
+    C.pw_hi_n = c->pw.p ? static_cast<uint32_t>(c->pw.count - 512) : 0;
     C.spm_ids = c->spm_ids.p;
     C.spm_vals = c->spm_vals.p;
     C.spm_tail = c->spm_tail.p;

@@ -66,13 +66,10 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
         double t[kChunks], e[kChunks];
 #pragma unroll
         for (int j = 0; j < kChunks; ++j) {
-            t[j] = 0.0;
-            e[j] = 0.0;
-            if ((f[j] >> lane) & 1u) {
-                const uint32_t v = (w + j) * 32 + lane;
-                t[j] = tau_of(v);
-                e[j] = eta_of(v);
-            }
+            const uint32_t v = (w + j) * 32 + lane;
+            const bool act = (f[j] >> lane) & 1u;
+            t[j] = tau_of(v, act);  // called by every lane (the SPM lookup shuffles)
+            e[j] = act ? eta_of(v) : 0.0;
         }
 #pragma unroll
         for (int j = 0; j < kChunks; ++j) {
@@ -232,10 +229,11 @@ __device__ __forceinline__ void closing_slots(const DevColony &C, uint32_t last,
 // SEQ parity test -- is bit-identical to the CAS/sequential result); c >= 2
 // uses the closed form tau0 + c_l^c (b - tau0) with c_l^c from two small
 // power tables (lo: c & 511, hi: c >> 9).
-__device__ __forceinline__ double trail_value(double b, uint32_t c, const DevColony &C) {
+__device__ __forceinline__ double trail_value(double b, uint32_t c, const DevColony &C,
+                                              const double *pw_lo, const double *pw_hi) {
     const double one = affine(b, C.c_l, C.c_0);
     double p = 1.0;
-    if (c >= 2u) p = __dmul_rn(__ldg(C.pw_lo + (c & 511u)), __ldg(C.pw_hi + (c >> 9)));
+    if (c >= 2u) p = __dmul_rn(pw_lo[c & 511u], pw_hi[c >> 9]);
     const double closed = __dadd_rn(C.tau_min, __dmul_rn(p, __dsub_rn(b, C.tau_min)));
     return c == 0u ? b : (c == 1u ? one : closed);
 }
@@ -269,8 +267,17 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
-    uint32_t *vis = reinterpret_cast<uint32_t *>(smem + wpb * 32 * sizeof(double)) +
+    // ATOMIC: c_l^c power tables staged in shared memory (the L1 is thrashed by
+    // the row stream, so a global-table lookup on the chain costs an L2 trip)
+    double *pw_lo = reinterpret_cast<double *>(smem) + wpb * 32;
+    double *pw_hi = pw_lo + 512;
+    const uint32_t pw_n = kAtomic ? 512 + C.pw_hi_n : 0;
+    uint32_t *vis = reinterpret_cast<uint32_t *>(smem + (wpb * 32 + pw_n) * sizeof(double)) +
                     static_cast<size_t>(wib) * I.words;
+    if constexpr (kAtomic) {
+        for (uint32_t i = threadIdx.x; i < pw_n; i += blockDim.x) pw_lo[i] = C.pw_lo[i];
+        __syncthreads();
+    }
     const uint64_t it = *C.iter;
     const uint32_t n = I.n;
     WarpCounters wc;
@@ -301,16 +308,20 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
         for (uint32_t t = 1; t < n; ++t) {
             Step st;
             if constexpr (kAtomic) {
-                const double tv = trail_value(tl, cl, C);
+                const double tv = trail_value(tl, cl, C, pw_lo, pw_hi);
                 select_step(I, C, vis, cur, el, tv, rng, la, scratch, lane,
-                            [&](uint32_t v) {
+                            [&](uint32_t v, bool act) {
+                                if (!act) return 0.0;
                                 const size_t k = static_cast<size_t>(cur) * n + v;
-                                return trail_value(ld_relaxed(C.tau + k), ld_relaxed_u32(C.cnt + k), C);
+                                return trail_value(ld_relaxed(C.tau + k), ld_relaxed_u32(C.cnt + k), C, pw_lo,
+                                                   pw_hi);
                             },
                             st);
             } else {
                 select_step(I, C, vis, cur, el, tl, rng, la, scratch, lane,
-                            [&](uint32_t v) { return ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v); },
+                            [&](uint32_t v, bool act) {
+                                return act ? ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v) : 0.0;
+                            },
                             st);
             }
             wc.count(st.kind, n - t);
@@ -393,14 +404,14 @@ __global__ void k_fold_counts(DevColony C, size_t dense_count, size_t cand_count
     for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < dense_count; i += stride) {
         const uint32_t c = C.cnt[i];
         if (c) {
-            C.tau[i] = trail_value(C.tau[i], c, C);
+            C.tau[i] = trail_value(C.tau[i], c, C, C.pw_lo, C.pw_hi);
             C.cnt[i] = 0;
         }
     }
     for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cand_count; i += stride) {
         const uint32_t c = C.cntc[i];
         if (c) {
-            C.tauc[i] = trail_value(C.tauc[i], c, C);
+            C.tauc[i] = trail_value(C.tauc[i], c, C, C.pw_lo, C.pw_hi);
             C.cntc[i] = 0;
         }
     }
@@ -408,14 +419,17 @@ __global__ void k_fold_counts(DevColony C, size_t dense_count, size_t cand_count
 
 // ============================================================ selective whole tour
 
-// Register copy of one record: every lane holds all S slots (broadcast loads).
+// Register copy of one record.  The S ids are in every lane (broadcast loads,
+// so the first-match search is local compares); the S values are spread one
+// per lane (lane j < S holds slot j) and fetched with one shuffle -- this keeps
+// the record at S + 3 registers per lane instead of 3S.
 template <int S>
 struct SpmRec {
     uint32_t id[S];
-    double val[S];
+    double val;     // slot `lane` (lanes < S)
     uint32_t tail;
 
-    __device__ __forceinline__ void load(const DevColony &C, uint32_t u) {
+    __device__ __forceinline__ void load(const DevColony &C, uint32_t u, int lane) {
         const size_t base = static_cast<size_t>(u) * S;
         if constexpr (S >= 4) {
 #pragma unroll
@@ -427,38 +441,30 @@ struct SpmRec {
 #pragma unroll
             for (int j = 0; j < S; ++j) id[j] = __ldcg(C.spm_ids + base + j);
         }
-        if constexpr (S >= 2) {
-#pragma unroll
-            for (int j = 0; j < S; j += 2) {
-                const double2 q = __ldcg(reinterpret_cast<const double2 *>(C.spm_vals + base + j));
-                val[j] = q.x; val[j + 1] = q.y;
-            }
-        } else {
-            val[0] = __ldcg(C.spm_vals + base);
-        }
+        val = lane < S ? __ldcg(C.spm_vals + base + lane) : 0.0;
         tail = __ldcg(C.spm_tail + u);
     }
-    __device__ __forceinline__ double lookup(uint32_t v, double tau_min) const {
-        double r = tau_min;
-        bool found = false;
-#pragma unroll
-        for (int j = 0; j < S; ++j)
-            if (!found && id[j] == v) { r = val[j]; found = true; }
-        return r;
-    }
-    // update record u with neighbour v; lane 0 writes through. Returns hit.
-    __device__ __forceinline__ bool update(const DevColony &C, uint32_t u, uint32_t v, double c_mul,
-                                           double c_add, int lane) {
+    __device__ __forceinline__ int find(uint32_t v) const {
         int hit = -1;
 #pragma unroll
-        for (int j = 0; j < S; ++j)
-            if (hit < 0 && id[j] == v) hit = j;
+        for (int j = S - 1; j >= 0; --j)
+            if (id[j] == v) hit = j;  // first (lowest) matching slot
+        return hit;
+    }
+    // tau of (u, v) for this lane's v; all lanes must call (warp shuffle)
+    __device__ __forceinline__ double lookup(uint32_t v, double tau_min) const {
+        const int hit = find(v);
+        const double x = __shfl_sync(kFull, val, hit < 0 ? 0 : hit);
+        return hit < 0 ? tau_min : x;
+    }
+    // update record u with neighbour v (warp-uniform); lane 0 writes through. Returns hit.
+    __device__ __forceinline__ bool update(const DevColony &C, uint32_t u, uint32_t v, double c_mul,
+                                           double c_add, int lane) {
+        const int hit = find(v);
         const size_t base = static_cast<size_t>(u) * S;
         if (hit >= 0) {
-            double y = 0.0;
-#pragma unroll
-            for (int j = 0; j < S; ++j)
-                if (j == hit) { y = affine(val[j], c_mul, c_add); val[j] = y; }
+            const double y = affine(__shfl_sync(kFull, val, hit), c_mul, c_add);
+            if (lane == hit) val = y;
             if (lane == 0) st_relaxed(C.spm_vals + base + hit, y);
             return true;
         }
@@ -466,7 +472,8 @@ struct SpmRec {
         const uint32_t t = (tail + 1) % S;
 #pragma unroll
         for (int j = 0; j < S; ++j)
-            if (j == static_cast<int>(t)) { id[j] = v; val[j] = y; }
+            if (j == static_cast<int>(t)) id[j] = v;
+        if (lane == static_cast<int>(t)) val = y;
         tail = t;
         if (lane == 0) {
             st_relaxed_u32(C.spm_ids + base + t, v);
@@ -496,7 +503,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
         const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));
         uint4 el = __ldg(C.rows + static_cast<size_t>(start) * 32 + lane);
         SpmRec<S> rec;
-        rec.load(C, start);
+        rec.load(C, start, lane);
         __syncwarp();
         if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
         __syncwarp();
@@ -514,7 +521,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
             const double tau_lane = rec.lookup(el.x & kIdMask, C.tau_min);
             Step st;
             select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
-                        [&](uint32_t v) { return rec.lookup(v, C.tau_min); }, st);
+                        [&](uint32_t v, bool act) { return rec.lookup(act ? v : kEmpty, C.tau_min); }, st);
             wc.count(st.kind, n - t);
             el = __ldg(C.rows + static_cast<size_t>(st.v) * 32 + lane);  // next row first
             pending = (++kc == C.k);
@@ -524,7 +531,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
                 if (rec.update(C, cur, st.v, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
                 prev = cur;
             }
-            rec.load(C, st.v);  // record of the next node
+            rec.load(C, st.v, lane);  // record of the next node
             if (st.kind == 0) rng.advance();
             la.prepare(rng);
             vis[st.v >> 5] |= 1u << (st.v & 31);
@@ -544,7 +551,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
             if (rec.update(C, cur, start, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
             __syncwarp();
             SpmRec<S> r2;
-            r2.load(C, start);
+            r2.load(C, start, lane);
             if (r2.update(C, start, cur, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
         }
         if (lane == 0) C.lens[a] = len + dclose;
@@ -689,7 +696,9 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
             la.prepare(rng);
             Step st;
             select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
-                        [&](uint32_t v) { return ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v); },
+                        [&](uint32_t v, bool act) {
+                            return act ? ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v) : 0.0;
+                        },
                         st);
             if (st.kind == 0) rng.advance();
             wc.count(st.kind, n - t);
@@ -896,17 +905,18 @@ __global__ void k_island_mask(const int64_t *key, int rank, const uint32_t *tour
 
 // ============================================================ launchers
 
-static size_t construct_smem(const DevInstance &I, int wpb) {
-    return static_cast<size_t>(wpb) * (32 * sizeof(double) + I.words * sizeof(uint32_t));
+static size_t construct_smem(const DevInstance &I, const DevColony &C, int wpb, bool pw) {
+    return static_cast<size_t>(wpb) * (32 * sizeof(double) + I.words * sizeof(uint32_t)) +
+           (pw ? (512 + C.pw_hi_n) * sizeof(double) : 0);
 }
 
 template <class K>
 static void launch_tour_kernel(K kernel, const DevInstance &I, const DevColony &C, bool one_warp,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool pw = false) {
     const int threads = one_warp ? 32 : kBlock;
     const int wpb = threads / 32;
     const unsigned grid = one_warp ? 1u : blocks_for(C.m, wpb);
-    const size_t smem = construct_smem(I, wpb);
+    const size_t smem = construct_smem(I, C, wpb, pw);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kernel<<<grid, threads, smem, s>>>(I, C);
@@ -928,8 +938,8 @@ void launch_construct(int variant, int rng, const DevInstance &I, const DevColon
     const bool philox = rng == ACS_RNG_PHILOX;
     switch (variant) {
         case ACS_VARIANT_ATOMIC:
-            if (philox) launch_tour_kernel(k_construct_dense<1, Philox>, I, C, false, s);
-            else launch_tour_kernel(k_construct_dense<1, Xoshiro>, I, C, false, s);
+            if (philox) launch_tour_kernel(k_construct_dense<1, Philox>, I, C, false, s, true);
+            else launch_tour_kernel(k_construct_dense<1, Xoshiro>, I, C, false, s, true);
             break;
         case ACS_VARIANT_RELAXED:
             if (philox) launch_tour_kernel(k_construct_dense<0, Philox>, I, C, false, s);
