@@ -11,7 +11,10 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libacs_b200.so")
+# ACS_LIB_VARIANT=<suffix> selects an in-tree A/B build libacs_b200_<suffix>.so
+# (kernel experiments); the default is the product library.
+_suffix = os.environ.get("ACS_LIB_VARIANT", "")
+LIB_PATH = os.path.join(HERE, f"libacs_b200_{_suffix}.so" if _suffix else "libacs_b200.so")
 
 ACS_OK, ACS_E_ARG, ACS_E_CUDA, ACS_E_NOMEM, ACS_E_NCCL, ACS_E_PARSE = 0, -1, -2, -3, -4, -5
 EUC_2D, CEIL_2D, ATT = 0, 1, 2

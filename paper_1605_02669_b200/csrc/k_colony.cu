@@ -299,10 +299,10 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
         long long len = 0;
         Lookahead<RNG> la;
         la.prepare(rng);
-        // RELAXED: the copy tauc[v][mirror] of edge (u,v) is written one step
-        // late, by the lane of row v whose candidate is u, from the value it
-        // just loaded -- row v is never written while its own load is in flight
-        // (u is visited, so the delay is invisible to this ant's selection).
+        // The copy tauc[v][mirror] of edge (u,v) is written one step late, by
+        // the lane of row v whose candidate is u (RELAXED: from the value it
+        // just loaded) -- row v is never written while its own load is in
+        // flight, and u is visited, so the delay is invisible to this ant.
         uint32_t mprev = kEmpty;
 
         for (uint32_t t = 1; t < n; ++t) {
@@ -325,25 +325,34 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
                             st);
             }
             wc.count(st.kind, n - t);
-            if constexpr (!kAtomic) {
-                if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev)
-                    st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
-                mprev = kEmpty;
+            // the copy of the previous edge in THIS row (v -> prev) is written now,
+            // by the lane holding prev, after the row's own load has completed
+            if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev) {
+                if constexpr (kAtomic) red_add1(C.cntc + static_cast<size_t>(cur) * 32 + lane);
+                else st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
             }
+            mprev = kEmpty;
+#ifdef ACS_EXP_LOAD_FIRST
+            const uint4 el_cur = el;
+            ri = static_cast<size_t>(st.v) * 32 + lane;
+            el = __ldg(C.rows + ri);
+            tl = ld_relaxed(C.tauc + ri);
+            if constexpr (kAtomic) cl = ld_relaxed_u32(C.cntc + ri);
+            (void)el_cur;
+#endif
             if (++kc == C.k) {  // D9 per-ant edge counter (warp-uniform)
                 kc = 0;
                 ++wc.updates;
                 bool dense;
                 size_t k;
-                if constexpr (kAtomic) {
-                    if (copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k))
-                        red_add1((dense ? C.cnt : C.cntc) + k);
-                } else {
-                    if (lane < 3 && copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k))
-                        st_relaxed((dense ? C.tau : C.tauc) + k, affine(st.tau_old, C.c_l, C.c_0));
-                    mprev = cur;
+                // lanes 0-2 now; lane 3's copy (tauc[v][mirror]) one step late, above
+                if (lane < 3 && copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k)) {
+                    if constexpr (kAtomic) red_add1((dense ? C.cnt : C.cntc) + k);
+                    else st_relaxed((dense ? C.tau : C.tauc) + k, affine(st.tau_old, C.c_l, C.c_0));
                 }
+                mprev = cur;
             }
+#ifndef ACS_EXP_LOAD_FIRST
             // Next dependent row load.  It is issued after this step's writes:
             // loading row v ahead of a write to the same line measured ~30%
             // slower per step on B200 (profiles/README.md).
@@ -351,6 +360,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
             el = __ldg(C.rows + ri);
             tl = ld_relaxed(C.tauc + ri);
             if constexpr (kAtomic) cl = ld_relaxed_u32(C.cntc + ri);
+#endif
             // commit a greedy step's q draw and peek the next one, off the chain
             if (st.kind == 0) rng.advance();
             la.prepare(rng);
@@ -362,9 +372,10 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
             __syncwarp();
         }
         route_flush(route, rbuf, n - 1, lane);
-        if constexpr (!kAtomic) {  // last step's deferred mirror copy (el/tl hold row `cur`)
-            if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev)
-                st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
+        // last step's deferred mirror copy (el/tl hold row `cur`)
+        if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev) {
+            if constexpr (kAtomic) red_add1(C.cntc + static_cast<size_t>(cur) * 32 + lane);
+            else st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
         }
         __syncwarp();
 
