@@ -332,14 +332,15 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
                 else st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
             }
             mprev = kEmpty;
-#ifdef ACS_EXP_LOAD_FIRST
-            const uint4 el_cur = el;
+            // Next dependent row load, issued as soon as v is known: the writes
+            // below touch rows u (tauc, tau) and v of the DENSE matrix only --
+            // the one copy in tauc row v is written a step late (above), because
+            // a write to the same line behind a pending load measured ~30%
+            // slower per step (profiles/README.md, v6).
             ri = static_cast<size_t>(st.v) * 32 + lane;
             el = __ldg(C.rows + ri);
             tl = ld_relaxed(C.tauc + ri);
             if constexpr (kAtomic) cl = ld_relaxed_u32(C.cntc + ri);
-            (void)el_cur;
-#endif
             if (++kc == C.k) {  // D9 per-ant edge counter (warp-uniform)
                 kc = 0;
                 ++wc.updates;
@@ -352,15 +353,6 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
                 }
                 mprev = cur;
             }
-#ifndef ACS_EXP_LOAD_FIRST
-            // Next dependent row load.  It is issued after this step's writes:
-            // loading row v ahead of a write to the same line measured ~30%
-            // slower per step on B200 (profiles/README.md).
-            ri = static_cast<size_t>(st.v) * 32 + lane;
-            el = __ldg(C.rows + ri);
-            tl = ld_relaxed(C.tauc + ri);
-            if constexpr (kAtomic) cl = ld_relaxed_u32(C.cntc + ri);
-#endif
             // commit a greedy step's q draw and peek the next one, off the chain
             if (st.kind == 0) rng.advance();
             la.prepare(rng);

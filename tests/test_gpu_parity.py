@@ -172,3 +172,11 @@ def test_atomic_single_ant_equals_seq(acs, orc, gpu):
     o = orc.run(I, m=1, iterations=8, seed=12, mode=O.SEQ, want_tau=True)
     assert st["global_best_len"].tolist() == o["trace"].tolist()
     assert np.array_equal(tau.view(np.uint64), o["tau"].view(np.uint64))
+
+
+def test_sync_more_ants_than_resident_warps(acs, orc, gpu):
+    """m > resident warps: the cooperative deferred kernel runs several ants
+    per warp (state in shared memory) and must stay bit-exact."""
+    I = O.load("d198")
+    r = pair(acs, orc, I, "sync", O.DENSE, m=3500, iters=2, seed=21)
+    check_exact(*r, O.DENSE)
