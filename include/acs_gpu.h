@@ -89,7 +89,8 @@ typedef struct {
     uint64_t greedy_steps, roulette_steps;
     uint64_t cas_retries;    /* atomic variant: failed CAS attempts */
     uint64_t iterations;     /* iterations run on this context */
-    uint64_t fallback_elems; /* unvisited nodes scanned by fallback steps */
+    uint64_t fallback_elems; /* unvisited nodes a full fallback scan covers (algorithmic) */
+    uint64_t fallback_full;  /* fallback steps the pruned pass could not settle (full scan run) */
 } acs_counters;
 
 typedef struct {

@@ -46,7 +46,8 @@ class Counters(C.Structure):
     _fields_ = [("local_updates", C.c_uint64), ("hits", C.c_uint64), ("misses", C.c_uint64),
                 ("fallback_steps", C.c_uint64), ("greedy_steps", C.c_uint64),
                 ("roulette_steps", C.c_uint64), ("cas_retries", C.c_uint64),
-                ("iterations", C.c_uint64), ("fallback_elems", C.c_uint64)]
+                ("iterations", C.c_uint64), ("fallback_elems", C.c_uint64),
+                ("fallback_full", C.c_uint64)]
 
 
 class CtxInfo(C.Structure):

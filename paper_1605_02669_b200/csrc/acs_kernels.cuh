@@ -24,6 +24,8 @@ struct DevInstance {
     const double *etab;  // n*n eta^beta (fallback scan operand) or nullptr
 };
 
+constexpr uint32_t kHot = 32;  // hot-list entries per row (one per lane)
+
 struct DevColony {
     uint32_t m, L, k, S;   // ants, list length, update period, spm slots
     double q0, beta;
@@ -33,6 +35,11 @@ struct DevColony {
     double tau_min;
     uint64_t seed;
     const uint4 *rows;     // n*32 packed candidate rows
+    const uint4 *ext;      // n*ext_len next-nearest rows {id, d, eta^beta} for the pruned fallback
+    uint32_t ext_len;      // multiple of 32, or 0
+    double tau_bound;      // tau0 * (1 + 2^-29): bound on every trail outside the hot lists
+    uint32_t *hot;         // n*kHot: non-candidate neighbours the global update deposited on
+    uint32_t *hot_cnt;     // n: entries used (> kHot: overflowed, full scan)
     double *tau;           // n*n dense, or nullptr
     double *tauc;          // n*32, or nullptr
     uint32_t *cnt;         // ATOMIC: n*n pending local updates of tau (tau = f^cnt(base))
@@ -51,7 +58,7 @@ struct DevColony {
 
 enum Counter {
     kCntUpdates = 0, kCntHits, kCntMisses, kCntFallback, kCntGreedy, kCntRoulette,
-    kCntCasRetry, kCntIters, kCntFallbackElems, kNumCounters = 16
+    kCntCasRetry, kCntIters, kCntFallbackElems, kCntFallbackFull, kNumCounters = 16
 };
 
 struct DevBest {
@@ -79,6 +86,11 @@ void launch_tour_lengths(const DevInstance &I, const uint32_t *routes, uint32_t 
                          cudaStream_t s);
 void launch_eta_table(const DevInstance &I, double beta, int beta_int, double *out,
                       cudaStream_t s);
+// extended neighbour rows (positions L .. L+ext_len-1 of each node's distance
+// order), ext_len a multiple of 32; scratch: n*32 keys + n lower bounds
+void launch_ext_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, uint32_t ext_len,
+                     double beta, int beta_int, uint64_t *scratch_keys, uint64_t *scratch_lower,
+                     uint4 *ext, cudaStream_t s);
 void launch_fill(double *p, size_t count, double value, cudaStream_t s);
 void launch_spm_init(uint32_t *ids, double *vals, uint32_t *tail, uint32_t n, uint32_t S,
                      double tau_min, cudaStream_t s);

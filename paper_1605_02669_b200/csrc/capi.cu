@@ -10,6 +10,10 @@
 #include <cstring>
 #include <algorithm>
 #include <memory>
+
+#ifndef ACS_EXT_MAX
+#define ACS_EXT_MAX 192u // next-nearest entries per row for the pruned fallback (multiple of 32)
+#endif
 #include <string>
 #include <vector>
 
@@ -167,7 +171,8 @@ struct acs_gpu_ctx {
     uint32_t n = 0, m = 0, L = 0, S = 0;
     double q0 = 0, tau0 = 0;
     int64_t nn_len = 0;
-    DBuf<uint4> rows;
+    DBuf<uint4> rows, ext;     // candidate rows; next-nearest rows for the pruned fallback
+    DBuf<uint32_t> hot, hot_cnt;  // per-row non-candidate edges the global update touched
     DBuf<uint32_t> cand;  // flat n*L (reference layout), kept for get_candidates
     DBuf<double> tau, tauc, spm_vals, etab, pw;
     DBuf<uint32_t> cnt, cntc;  // ATOMIC variant: pending local updates per copy
@@ -205,7 +210,7 @@ struct acs_gpu_ctx {
         return ACS_OK;
     }
     size_t device_bytes() const {
-        return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + etab.bytes() + rows.bytes() + cand.bytes() +
+        return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + etab.bytes() + rows.bytes() + ext.bytes() + hot.bytes() + hot_cnt.bytes() + cand.bytes() +
                tau.bytes() + tauc.bytes() + spm_vals.bytes() + spm_ids.bytes() + spm_tail.bytes() +
                routes.bytes() + best_tour.bytes() + lens.bytes() + cnt.bytes() + cntc.bytes();
     }
@@ -410,6 +415,20 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     launch_topk(I, c->L, c->cand.p, s);
     launch_build_rows(I, c->cand.p, c->L, p->beta, bint, c->rows.p, s);
     CUDA_TRY(cudaGetLastError());
+    // next-nearest rows after the candidate list (pruned exact fallback scan)
+    {
+        const uint32_t rest = n - 1 - c->L;
+        const uint32_t ext_len = std::min<uint32_t>(ACS_EXT_MAX, (rest + 31) / 32 * 32);
+        if (ext_len) {
+            DBuf<uint64_t> keys, lower;
+            CUDA_TRY(keys.alloc(static_cast<size_t>(n) * 32));
+            CUDA_TRY(lower.alloc(n));
+            CUDA_TRY(c->ext.alloc(static_cast<size_t>(n) * ext_len));
+            launch_ext_rows(I, c->cand.p, c->L, ext_len, p->beta, bint, keys.p, lower.p, c->ext.p, s);
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaStreamSynchronize(s));
+        }
+    }
     // tau0 = 1/(n * L_nn) from the NN tour from node 0
     CUDA_TRY(c->best_len.alloc(1));
     launch_nn_tour(I, 0, c->best_len.p, s);
@@ -493,6 +512,16 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     C.tau_min = c->tau0;
     C.seed = p->seed;
     C.rows = c->rows.p;
+    C.ext = c->ext.p;
+    C.ext_len = c->ext.p ? static_cast<uint32_t>(c->ext.count / n) : 0;
+    C.tau_bound = c->tau0 * (1.0 + 0x1.0p-29);
+    if (C.ext_len) {
+        CUDA_TRY(c->hot.alloc(static_cast<size_t>(n) * kHot));
+        CUDA_TRY(c->hot_cnt.alloc(n));
+        CUDA_TRY(cudaMemsetAsync(c->hot_cnt.p, 0, n * sizeof(uint32_t), s));
+        C.hot = c->hot.p;
+        C.hot_cnt = c->hot_cnt.p;
+    }
     C.tau = c->tau.p;
     C.tauc = c->tauc.p;
     C.cnt = c->cnt.p;
@@ -670,6 +699,7 @@ int acs_gpu_get_counters(const acs_gpu_ctx *c, acs_counters *o) {
     o->cas_retries = h[kCntCasRetry];
     o->iterations = h[kCntIters];
     o->fallback_elems = h[kCntFallbackElems];
+    o->fallback_full = h[kCntFallbackFull];
     return ACS_OK;
 }
 

@@ -40,6 +40,61 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
                                               const uint32_t *vis, uint32_t cur, TauFn tau_of,
                                               int lane, Step &o) {
     const double xc = __ldg(I.xs + cur), yc = __ldg(I.ys + cur);
+    // Exact pruned pass.  Only the global update raises a trail above tau0
+    // (local updates move it towards tau0), and every non-candidate edge it
+    // ever touched is in cur's hot list.  So: score the hot list exactly, then
+    // walk the next-nearest neighbours in distance order; once
+    // tau_bound * eta^beta(last scanned) < best, no unscanned node can win or
+    // tie, and the result equals the full scan's (argmax, ties -> lowest id).
+    const uint32_t hcnt = C.ext_len ? __ldg(C.hot_cnt + cur) : kHot + 1;
+    if (hcnt <= kHot) {
+        double bs = 0.0, bt = 0.0;
+        uint32_t bv = 0xffffffffu;
+        bool have = false;
+        {
+            const bool in_list = static_cast<uint32_t>(lane) < hcnt;
+            const uint32_t v = in_list ? __ldg(C.hot + static_cast<size_t>(cur) * kHot + lane) : 0u;
+            const bool act = in_list && !visited(vis, v);
+            const double tv = tau_of(v, act);
+            if (act) {
+                const double e = I.etab ? __ldg(I.etab + static_cast<size_t>(cur) * I.n + v)
+                                        : eta_beta(tsplib_distance(I.type, xc, yc, __ldg(I.xs + v), __ldg(I.ys + v)),
+                                                   C.beta, C.beta_int);
+                have = true; bs = __dmul_rn(tv, e); bv = v; bt = tv;
+            }
+        }
+        const uint4 *xrow = C.ext + static_cast<size_t>(cur) * C.ext_len;
+        for (uint32_t base = 0; base < C.ext_len; base += 32) {
+            const uint4 q = __ldg(xrow + base + lane);
+            const bool in_list = q.x != kEmpty;
+            const bool act = in_list && !visited(vis, q.x);
+            const double tv = tau_of(in_list ? q.x : 0u, act);
+            if (act) {
+                const double sc = __dmul_rn(tv, __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z)));
+                if (!have || sc > bs || (sc == bs && q.x < bv)) { have = true; bs = sc; bv = q.x; bt = tv; }
+            }
+            double sb = bs;
+            uint32_t node = have ? bv : 0xffffffffu;
+            warp_argmax_node(sb, node, have);
+            // the list ends inside this slice: every non-candidate node was scanned
+            const bool exhausted = __any_sync(kFull, !in_list);
+            const uint32_t lw = __shfl_sync(kFull, q.w, 31), lz = __shfl_sync(kFull, q.z, 31);
+            const double bound = __dmul_rn(C.tau_bound, __hiloint2double(static_cast<int>(lw), static_cast<int>(lz)));
+            if (node != 0xffffffffu && (exhausted || bound < sb)) {
+                const unsigned owner = __ballot_sync(kFull, have && bv == node);
+                o.v = node;
+                o.tau_old = __shfl_sync(kFull, bt, __ffs(owner) - 1);
+                o.d = tsplib_distance(I.type, xc, yc, __ldg(I.xs + node), __ldg(I.ys + node));
+                o.pos = -1;
+                o.kind = 2;
+                const uint32_t id = __ldg(&C.rows[static_cast<size_t>(node) * 32 + lane].x) & kIdMask;
+                const unsigned mm = __ballot_sync(kFull, static_cast<uint32_t>(lane) < C.L && id == cur);
+                o.mirror = mm ? static_cast<uint32_t>(__ffs(mm) - 1) : kNoMirror;
+                return;
+            }
+        }
+    }
+    if (lane == 0) atomicAdd(C.counters + kCntFallbackFull, 1ull);
     const double *erow = I.etab ? I.etab + static_cast<size_t>(cur) * I.n : nullptr;
     auto eta_of = [&](uint32_t v) -> double {
         if (erow) return __ldg(erow + v);
@@ -831,6 +886,20 @@ __global__ void __launch_bounds__(1024) k_best(DevColony C, DevBest B, uint32_t 
     }
 }
 
+// Record v in u's hot list (non-candidate neighbours whose trail the global
+// update raised above tau0).  Tour edges are distinct, so no two threads insert
+// the same (u, v) concurrently; an earlier iteration's insert is visible here.
+// Past kHot entries the row is marked full and its fallback scans everything.
+__device__ __forceinline__ void hot_insert(const DevColony &C, uint32_t u, uint32_t v) {
+    const uint32_t have = C.hot_cnt[u];
+    const uint32_t *h = C.hot + static_cast<size_t>(u) * kHot;
+    for (uint32_t i = 0; i < min(have, kHot); ++i)
+        if (h[i] == v) return;
+    if (have > kHot) return;
+    const uint32_t slot = atomicAdd(C.hot_cnt + u, 1u);
+    if (slot < kHot) C.hot[static_cast<size_t>(u) * kHot + slot] = v;
+}
+
 // dense global update, warp per global-best edge (a,b): lanes 0-3 update the
 // four copies of the trail; tour edges are distinct, so no two warps touch
 // the same word.
@@ -854,6 +923,10 @@ __global__ void k_global_dense(DevInstance I, DevColony C, DevBest B) {
     }
     double *p = copy_addr(C, n, a, b, pos, mirror, lane);
     if (p) *p = affine(*p, B.c_g, c_d);
+    if (C.hot && lane == 0) {
+        if (pos < 0) hot_insert(C, a, b);
+        if (mirror == kNoMirror) hot_insert(C, b, a);
+    }
 }
 
 // selective global update, thread per record r = tour[j]: edge j-1 (b-side,
@@ -872,6 +945,16 @@ __global__ void k_global_spm(DevInstance I, DevColony C, DevBest B) {
         const uint32_t second = j == 0 ? nb_prev : nb_next;
         if (spm_update_mem(C.spm_ids, C.spm_vals, C.spm_tail, C.S, r, first, B.c_g, c_d, C.tau_min, nullptr)) ++hits; else ++misses;
         if (spm_update_mem(C.spm_ids, C.spm_vals, C.spm_tail, C.S, r, second, B.c_g, c_d, C.tau_min, nullptr)) ++hits; else ++misses;
+        if (C.hot) {
+            bool in1 = false, in2 = false;
+            for (uint32_t l = 0; l < C.L; ++l) {
+                const uint32_t id = __ldg(&C.rows[static_cast<size_t>(r) * 32 + l].x) & kIdMask;
+                in1 |= id == first;
+                in2 |= id == second;
+            }
+            if (!in1) hot_insert(C, r, first);
+            if (!in2) hot_insert(C, r, second);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

@@ -75,6 +75,63 @@ __global__ void __launch_bounds__(kBlock) k_topk(DevInstance I, uint32_t L, uint
     if (static_cast<uint32_t>(lane) < L) out[static_cast<size_t>(u) * L + lane] = static_cast<uint32_t>(top);
 }
 
+// K2': the 32 smallest keys of node u STRICTLY above lower[u] -- successive
+// 32-slices of u's distance order (the extended neighbour list of the exact
+// pruned fallback scan).  Same warp merge as k_topk.
+__global__ void __launch_bounds__(kBlock) k_topk_after(DevInstance I, const uint64_t *lower,
+                                                      uint64_t *keys_out) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t u = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (u >= I.n) return;
+    const double xu = __ldg(I.xs + u), yu = __ldg(I.ys + u);
+    const uint64_t lo = lower[u];
+    uint64_t top = ~0ull;
+    for (uint32_t base = 0; base < I.n; base += 32) {
+        const uint32_t v = base + lane;
+        uint64_t key = ~0ull;
+        if (v < I.n && v != u) {
+            const int32_t d = tsplib_distance(I.type, xu, yu, __ldg(I.xs + v), __ldg(I.ys + v));
+            key = (static_cast<uint64_t>(static_cast<uint32_t>(d)) << 32) | v;
+            if (key <= lo) key = ~0ull;
+        }
+        const uint64_t thr = shfl_u64(top, 31);
+        if (!__any_sync(kFull, key < thr)) continue;
+        key = warp_sort_u64(key, lane);
+        const uint64_t rev = shfl_u64(key, 31 - lane);
+        top = top < rev ? top : rev;
+        top = warp_merge_u64(top, lane);
+    }
+    keys_out[static_cast<size_t>(u) * 32 + lane] = top;
+}
+
+// key of the last candidate of every node: the lower bound of the first slice
+__global__ void k_last_cand_key(DevInstance I, const uint32_t *cand, uint32_t L, uint64_t *lower) {
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= I.n) return;
+    const uint32_t c = cand[static_cast<size_t>(u) * L + L - 1];
+    const int32_t d = tsplib_distance(I.type, I.xs[u], I.ys[u], I.xs[c], I.ys[c]);
+    lower[u] = (static_cast<uint64_t>(static_cast<uint32_t>(d)) << 32) | c;
+}
+
+// slice j of the extended rows {id, d, eta^beta lo, hi} (id = kEmpty past the end);
+// also advances lower[u] to the slice's last key
+__global__ void k_ext_rows(DevInstance I, const uint64_t *keys, uint32_t j, uint32_t ext_len,
+                           double beta, int beta_int, uint4 *ext, uint64_t *lower) {
+    const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<size_t>(I.n) * 32) return;
+    const uint32_t u = static_cast<uint32_t>(idx >> 5), p = static_cast<uint32_t>(idx & 31);
+    const uint64_t key = keys[idx];
+    uint4 el = make_uint4(kEmpty, 0u, 0u, 0u);
+    if (key != ~0ull) {
+        const int32_t d = static_cast<int32_t>(key >> 32);
+        const uint64_t b = dbits(eta_beta(d, beta, beta_int));
+        el = make_uint4(static_cast<uint32_t>(key), static_cast<uint32_t>(d), static_cast<uint32_t>(b),
+                        static_cast<uint32_t>(b >> 32));
+    }
+    ext[static_cast<size_t>(u) * ext_len + j * 32 + p] = el;
+    if (p == 31) lower[u] = key;
+}
+
 // packed candidate rows: {id | mirror<<24, d, eta^beta lo, eta^beta hi}
 __global__ void k_build_rows(DevInstance I, const uint32_t *cand, uint32_t L, double beta,
                              int beta_int, uint4 *rows) {
@@ -281,6 +338,17 @@ void launch_spm_script(uint32_t *ids, double *vals, uint32_t *tail, uint32_t S, 
                        unsigned long long *hits_misses, cudaStream_t s) {
     k_spm_script<<<1, 1, 0, s>>>(ids, vals, tail, S, tau_min, c_l, c_0, alpha, c_g, ops, lgb,
                                  count, out, hits_misses);
+}
+
+void launch_ext_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, uint32_t ext_len,
+                     double beta, int beta_int, uint64_t *scratch_keys, uint64_t *scratch_lower,
+                     uint4 *ext, cudaStream_t s) {
+    k_last_cand_key<<<blocks_for(I.n, 256), 256, 0, s>>>(I, cand, L, scratch_lower);
+    for (uint32_t j = 0; j * 32 < ext_len; ++j) {
+        k_topk_after<<<blocks_for(I.n, kWarpsPerBlock), kBlock, 0, s>>>(I, scratch_lower, scratch_keys);
+        k_ext_rows<<<blocks_for(static_cast<size_t>(I.n) * 32, 256), 256, 0, s>>>(
+            I, scratch_keys, j, ext_len, beta, beta_int, ext, scratch_lower);
+    }
 }
 
 void launch_eta_table(const DevInstance &I, double beta, int beta_int, double *out,
