@@ -49,6 +49,12 @@ def parse_args():
     return ap.parse_args()
 
 
+def data_desc(name: str) -> str:
+    if name.startswith("rnd"):
+        return f"synthetic {name}: uniform integer coordinates in [0,1e6)^2 from RngStream(20161017)"
+    return f"TSPLIB {name} (real instance, data/tsplib)"
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -138,12 +144,14 @@ def cpu_baseline_seq(name: str, m: int, k: int):
     """oracle SEQ (ACS-SEQ restated) on one host core, bounded sample."""
     import oracle as O
     I = O.load(name)
-    iters = 3
-    o = O.Oracle().run(I, m=m, iterations=iters, seed=0, mode=O.SEQ, k=k, want_routes=False)
-    tps = m * iters / (o["loop_ms"] / 1e3)
+    # bounded sample (~5-20 s of one core): 3 full iterations up to pr2392,
+    # one iteration of a 1000-ant colony beyond
+    iters, m_s = (3, m) if I.n <= 4096 else (1, min(m, 1000))
+    o = O.Oracle().run(I, m=m_s, iterations=iters, seed=0, mode=O.SEQ, k=k, want_routes=False)
+    tps = m_s * iters / (o["loop_ms"] / 1e3)
     return {"value": round(tps, 1), "unit": "tours/s", "cores": 1, "kind": "port",
-            "sample": f"oracle SEQ (ant-major, immediate updates) on {name}, m={m}, k={k}, "
-                      f"{iters} iterations = {m * iters} tours, {o['loop_ms'] / 1e3:.1f} s"}
+            "sample": f"oracle SEQ (ant-major, immediate updates) on {name}, m={m_s}, k={k}, "
+                      f"{iters} iterations = {m_s * iters} tours, {o['loop_ms'] / 1e3:.1f} s"}
 
 
 def run_reference(args):
@@ -178,7 +186,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "tours/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(sum(loop_ms) / args.steps * m / m_step, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": f"TSPLIB {args.instance} (real instance)",
+        "vs_baseline": None, "dtype": "f64", "data": data_desc(args.instance),
         "config": {"workload": f"{args.instance} ACS, {m} ants, cl=32, k={args.k}, {args.variant}",
                    "variant": args.variant, "mode": ["seq", "sync", "relaxed"][mode],
                    "memory": ["dense", "selective"][memory], "consistent": consistent},
@@ -199,7 +207,6 @@ def main():
     rank, world, local = dist_env()
     import numpy as np
     import torch
-    import oracle as O  # data files + optimum catalog only (no oracle compute here)
     import paper_1605_02669_b200 as P
 
     torch.cuda.set_device(local)
@@ -208,9 +215,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    I = O.load(args.instance)
-    opt = O.optima().get(args.instance)
-    inst = P.TspInstance(I.name, I.type, I.xs.copy(), I.ys.copy(), opt)
+    inst = P.load_instance(args.instance)
+    opt = inst.optimum
     m = args.ants or inst.n
     # P11: colony c uses seed + c * golden -> colony 0 == the single-GPU run
     seed = (args.seed + rank * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
@@ -281,7 +287,7 @@ def main():
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": round(value / PAPER_ACS_GPU_PR2392, 2) if args.instance == "pr2392" and args.variant == "atomic" else None,
         "vs_baseline_ref": "paper ACS-GPU (atomic) pr2392 4942 tours/s on GK104 (BASELINE.md, PAPER.md:920)",
-        "dtype": "f64", "data": f"TSPLIB {args.instance} (real instance, data/tsplib)",
+        "dtype": "f64", "data": data_desc(args.instance),
         "config": {"workload": f"{args.instance} ACS, {m} ants, cl=32, k={args.k}, {args.variant} dense"
                    if args.variant != "spm" else f"{args.instance} ACS-SPM, {m} ants, s=8",
                    "instance": args.instance, "n": inst.n, "ants_per_gpu": m, "variant": args.variant,

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ACS_GPU_ABI_VERSION 1
+#define ACS_GPU_ABI_VERSION 2  /* 2: acs_counters.fallback_full, acs_random_instance */
 
 /* status codes */
 #define ACS_OK 0
@@ -112,6 +112,10 @@ int acs_gpu_device_count(int *count);
  * return ACS_E_PARSE with the reference's field-naming message. */
 int acs_parse_tsplib(const char *text, size_t len, uint32_t *n, uint32_t *edge_weight_type,
                      double *xs, double *ys, uint32_t cap, char *name, size_t name_cap);
+
+/* synthetic uniform instance: coordinates drawn by the
+ * reference RngStream(seed).uniform_int(side) (rng.hpp:16-84), x then y per node */
+int acs_random_instance(uint32_t n, uint64_t seed, uint32_t side, double *xs, double *ys);
 
 /* ---- stateless device ops (setup path) ----
  * replaces TspInstance ctor's dist_table_ (tsp_instance.cpp:23-47) */

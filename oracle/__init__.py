@@ -82,6 +82,8 @@ def parse_coords(text: str) -> Coords:
 
 
 def load(name: str) -> Coords:
+    if name.startswith("rnd") and name[3:].rstrip("k").isdigit():
+        return rnd_instance(int(name[3:-1]) * 1000 if name.endswith("k") else int(name[3:]))
     return parse_coords(read_tsplib_text(name))
 
 

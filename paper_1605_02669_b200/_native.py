@@ -67,6 +67,7 @@ SIGNATURES = {
     "acs_gpu_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "acs_parse_tsplib": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(_u32), C.POINTER(_u32), _P, _P,
                                    _u32, C.c_char_p, C.c_size_t]),
+    "acs_random_instance": (C.c_int, [_u32, _u64, _u32, _P, _P]),
     "acs_gpu_distance_table": (C.c_int, [_desc, C.c_int, _P]),
     "acs_gpu_build_candidates": (C.c_int, [_desc, _u32, C.c_int, _P, C.POINTER(_u32)]),
     "acs_gpu_nn_tour_length": (C.c_int, [_desc, _u32, C.c_int, C.POINTER(_i64)]),

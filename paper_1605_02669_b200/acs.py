@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import gzip
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Optional
@@ -96,6 +97,51 @@ def load_tsplib_file(path: str) -> TspInstance:
     except OSError:
         raise ParseError(f"cannot open instance file: {path}") from None
     return parse_tsplib(text)
+
+
+# instance files shipped with the repo (gzipped TSPLIB + the optimum catalog)
+DATA_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "data", "tsplib")
+
+
+def load_optimum_catalog_file(path: str) -> dict:
+    """name -> optimal length (reference load_optimum_catalog_file, cpp:282-305)."""
+    opener = gzip.open if path.endswith(".gz") else open
+    out = {}
+    try:
+        with opener(path, "rt") as f:
+            for line in f:
+                fields = line.split("#", 1)[0].split()
+                if len(fields) >= 2:
+                    out[fields[0]] = int(fields[1])
+    except OSError:
+        raise RuntimeError(f"cannot open optimum catalog: {path}") from None
+    return out
+
+
+def optima() -> dict:
+    return load_optimum_catalog_file(os.path.join(DATA_DIR, "optima.txt.gz"))
+
+
+def random_uniform_instance(n: int, seed: int = 20161017, side: int = 1000000) -> TspInstance:
+    """integer coordinates uniform in [0, side)^2 from the
+    reference RngStream(seed).uniform_int(side), x then y per node."""
+    xs = np.empty(n, np.float64)
+    ys = np.empty(n, np.float64)
+    N.check(N.lib().acs_random_instance(n, seed, side, _ptr(xs), _ptr(ys)), "random_instance")
+    name = f"rnd{n // 1000}k" if n % 1000 == 0 else f"rnd{n}"
+    return TspInstance(name, N.EUC_2D, xs, ys)
+
+
+def load_instance(name: str) -> TspInstance:
+    """A shipped TSPLIB instance by name (data/tsplib/<name>.tsp.gz), or a
+    synthetic ``rnd<k>k`` / ``rnd<n>`` instance; the optimum is attached when
+    the catalog has it."""
+    if name.startswith("rnd") and name[3:].rstrip("k").isdigit():
+        n = int(name[3:-1]) * 1000 if name.endswith("k") else int(name[3:])
+        return random_uniform_instance(n)
+    inst = load_tsplib_file(os.path.join(DATA_DIR, f"{name}.tsp.gz"))
+    inst.optimum = optima().get(inst.name)
+    return inst
 
 
 @dataclass

@@ -14,6 +14,7 @@
 #include <sstream>
 
 #include "../../include/acs/instance.hpp"
+#include "../../include/acs/rng_stream.hpp"
 
 void acs_set_error(const char *msg);  // capi.cu: thread-local ABI error
 
@@ -238,7 +239,29 @@ std::map<std::string, int64_t> load_optimum_catalog_file(const std::string &path
     return load_optimum_catalog(in);
 }
 
+TspInstance random_uniform_instance(uint32_t n, uint64_t seed, uint32_t side) {
+    RngStream rng(seed);
+    std::vector<double> xs(n), ys(n);
+    for (uint32_t i = 0; i < n; ++i) {  // x then y per node, sequenced draws
+        xs[i] = static_cast<double>(rng.uniform_int(side));
+        ys[i] = static_cast<double>(rng.uniform_int(side));
+    }
+    std::string name = n % 1000 == 0 ? "rnd" + std::to_string(n / 1000) + "k" : "rnd" + std::to_string(n);
+    return TspInstance(std::move(name), EdgeWeightType::kEuc2d, std::move(xs), std::move(ys));
+}
+
 }  // namespace acs
+
+extern "C" int acs_random_instance(uint32_t n, uint64_t seed, uint32_t side, double *xs, double *ys) {
+    if (n < 3 || side == 0 || !xs || !ys) {
+        acs_set_error("acs_random_instance: need n >= 3, side >= 1 and output buffers");
+        return ACS_E_ARG;
+    }
+    const acs::TspInstance inst = acs::random_uniform_instance(n, seed, side);
+    std::memcpy(xs, inst.xs_.data(), sizeof(double) * n);
+    std::memcpy(ys, inst.ys_.data(), sizeof(double) * n);
+    return ACS_OK;
+}
 
 // ---- C-ABI: TSPLIB text -> caller storage ----
 extern "C" int acs_parse_tsplib(const char *text, size_t len, uint32_t *n, uint32_t *type,
