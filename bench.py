@@ -41,6 +41,9 @@ def parse_args():
     ap.add_argument("--variant", default="atomic")
     ap.add_argument("--ants", type=int, default=0)
     ap.add_argument("--k", type=int, default=1)
+    ap.add_argument("--rng", default="auto", choices=["auto", "philox", "xoshiro"],
+                    help="per-ant stream of the GPU arm; auto = philox (counter-based, 32 draws per "
+                         "warp evaluation) for atomic/relaxed, xoshiro (the reference RngStream) otherwise")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--exchange-every", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,6 +202,12 @@ def run_reference(args):
     return 0
 
 
+def rng_for(variant: str, rng: str) -> str:
+    if rng != "auto":
+        return rng
+    return "philox" if variant in ("atomic", "relaxed") else "xoshiro"
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
@@ -220,7 +229,7 @@ def main():
     m = args.ants or inst.n
     # P11: colony c uses seed + c * golden -> colony 0 == the single-GPU run
     seed = (args.seed + rank * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
-    params = P.AcsParams(variant=args.variant, m=m, k=args.k, seed=seed)
+    params = P.AcsParams(variant=args.variant, m=m, k=args.k, seed=seed, rng=rng_for(args.variant, args.rng))
     col = P.Colony(inst, params, device=local)
     if world > 1:
         uid = [P.Colony.nccl_unique_id() if rank == 0 else None]
@@ -292,7 +301,7 @@ def main():
                    if args.variant != "spm" else f"{args.instance} ACS-SPM, {m} ants, s=8",
                    "instance": args.instance, "n": inst.n, "ants_per_gpu": m, "variant": args.variant,
                    "cl": 32, "k": args.k, "beta": 3.0, "alpha": 0.2, "rho": 0.01,
-                   "q0": round(col.info.q0, 6), "l2": "flushed (256 MiB write) before every timed step",
+                   "q0": round(col.info.q0, 6), "rng": rng_for(args.variant, args.rng), "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": f"island x{world}" if world > 1 else "single colony",
                    "exchange_every": args.exchange_every if world > 1 else None},
         "roofline": roofline,
@@ -327,7 +336,7 @@ def other_variants(P, inst, args, device):
     for v in ("atomic", "relaxed", "spm", "deferred"):
         if v == args.variant:
             continue
-        p = P.AcsParams(variant=v, m=args.ants or inst.n, k=args.k, seed=args.seed)
+        p = P.AcsParams(variant=v, m=args.ants or inst.n, k=args.k, seed=args.seed, rng=rng_for(v, args.rng))
         with P.Colony(inst, p, device=device) as col:
             col.iterate(2)
             ms = []

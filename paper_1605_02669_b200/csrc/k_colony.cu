@@ -162,7 +162,64 @@ struct Lookahead {
         q53 = rng.peek() >> 11;
         asm volatile("" : "+l"(q53));  // keep it here: no rematerialisation on the chain
     }
+    __device__ __forceinline__ bool greedy(const DevColony &C) const { return q53 <= C.q0_k; }
 };
+
+// Philox4x32-10 evaluated 32 draws at a time, one per lane, for a warp that
+// owns one ant.  Draw j of (seed, iteration, ant) is Philox::peek() at draw
+// j, so the stream is bit-identical to the scalar engine (and to the oracle's
+// PHILOX mode); what changes is the cost: one Philox evaluation per 32 draws
+// instead of one per draw, and the q <= q0 test of every draw of the batch is
+// a single ballot (qmask), so a greedy step reads one bit.
+struct PhiloxWarp {
+    Philox key;         // (seed, iteration, ant); key.draw unused
+    uint64_t q0_k;
+    uint64_t mine;      // draw base + lane
+    uint32_t base, draw, qmask;
+
+    __device__ __forceinline__ void fill() {
+        Philox p = key;
+        p.draw = base + (threadIdx.x & 31u);
+        mine = p.peek();
+        qmask = __ballot_sync(kFull, (mine >> 11) <= q0_k);
+    }
+    __device__ __forceinline__ void derive(uint64_t seed, uint64_t it, uint64_t a, uint64_t q0k) {
+        key.derive(seed, it, a);
+        q0_k = q0k;
+        base = draw = 0;
+        fill();
+    }
+    __device__ __forceinline__ uint64_t peek() const { return shfl_u64(mine, static_cast<int>(draw - base)); }
+    __device__ __forceinline__ void advance() {
+        if (++draw - base == 32u) {  // warp-uniform, once per 32 draws
+            base += 32u;
+            fill();
+        }
+    }
+    __device__ __forceinline__ uint64_t next() {
+        const uint64_t r = peek();
+        advance();
+        return r;
+    }
+    __device__ __forceinline__ bool greedy_bit() const { return (qmask >> (draw - base)) & 1u; }
+};
+
+template <>
+struct Lookahead<PhiloxWarp> {
+    bool g;
+    __device__ __forceinline__ void prepare(const PhiloxWarp &rng) { g = rng.greedy_bit(); }
+    __device__ __forceinline__ bool greedy(const DevColony &) const { return g; }
+};
+
+// per-ant stream of a construction warp
+template <class RNG>
+__device__ __forceinline__ void rng_init(RNG &rng, const DevColony &C, uint64_t it, uint64_t a) {
+    rng.derive(C.seed, it, a);
+}
+template <>
+__device__ __forceinline__ void rng_init(PhiloxWarp &rng, const DevColony &C, uint64_t it, uint64_t a) {
+    rng.derive(C.seed, it, a, C.q0_k);
+}
 
 // Candidate branch (Eq.1 / Eq.2 over the filtered list, Alg.2 l.5-16) with the
 // P1 draw protocol; falls through to fallback_scan when all are visited.
@@ -182,7 +239,7 @@ __device__ __forceinline__ void select_step(const DevInstance &I, const DevColon
         const double eb = __hiloint2double(static_cast<int>(el.w), static_cast<int>(el.z));
         const double score = unv ? __dmul_rn(tau_lane, eb) : 0.0;
         int pos;
-        if (la.q53 <= C.q0_k) {
+        if (la.greedy(C)) {
             pos = warp_argmax_pos(score, unv);
             o.kind = 0;
         } else {
@@ -340,7 +397,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
     for (uint32_t a = blockIdx.x * wpb + wib; a < C.m; a += gridDim.x * wpb) {
         for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
         RNG rng;
-        rng.derive(C.seed, it, a);
+        rng_init(rng, C, it, a);
         const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));  // P1.1
         size_t ri = static_cast<size_t>(start) * 32 + lane;
         uint4 el = __ldg(C.rows + ri);
@@ -379,7 +436,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony
                             },
                             st);
             }
-            wc.count(st.kind, n - t);
+            if (st.kind) wc.count(st.kind, n - t);  // greedy steps are derived at flush
             // the copy of the previous edge in THIS row (v -> prev) is written now,
             // by the lane holding prev, after the row's own load has completed
             if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev) {
@@ -557,7 +614,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
     for (uint32_t a = blockIdx.x * wpb + wib; a < C.m; a += gridDim.x * wpb) {
         for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
         RNG rng;
-        rng.derive(C.seed, it, a);
+        rng_init(rng, C, it, a);
         const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));
         uint4 el = __ldg(C.rows + static_cast<size_t>(start) * 32 + lane);
         SpmRec<S> rec;
@@ -724,7 +781,7 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
         uint32_t *vis = vis_base + j * I.words;
         for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
         RNG rng;
-        rng.derive(C.seed, it, a);
+        rng_init(rng, C, it, a);
         const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));
         __syncwarp();
         if (lane == 0) {
@@ -1024,20 +1081,20 @@ void launch_construct(int variant, int rng, const DevInstance &I, const DevColon
     const bool philox = rng == ACS_RNG_PHILOX;
     switch (variant) {
         case ACS_VARIANT_ATOMIC:
-            if (philox) launch_tour_kernel(k_construct_dense<1, Philox>, I, C, false, s, true);
+            if (philox) launch_tour_kernel(k_construct_dense<1, PhiloxWarp>, I, C, false, s, true);
             else launch_tour_kernel(k_construct_dense<1, Xoshiro>, I, C, false, s, true);
             break;
         case ACS_VARIANT_RELAXED:
-            if (philox) launch_tour_kernel(k_construct_dense<0, Philox>, I, C, false, s);
+            if (philox) launch_tour_kernel(k_construct_dense<0, PhiloxWarp>, I, C, false, s);
             else launch_tour_kernel(k_construct_dense<0, Xoshiro>, I, C, false, s);
             break;
         case ACS_VARIANT_SEQ:
-            if (philox) launch_tour_kernel(k_construct_dense<0, Philox>, I, C, true, s);
+            if (philox) launch_tour_kernel(k_construct_dense<0, PhiloxWarp>, I, C, true, s);
             else launch_tour_kernel(k_construct_dense<0, Xoshiro>, I, C, true, s);
             break;
         case ACS_VARIANT_SPM:
         case ACS_VARIANT_SPM_SEQ:
-            if (philox) launch_spm_rng<Philox>(I, C, variant == ACS_VARIANT_SPM_SEQ, s);
+            if (philox) launch_spm_rng<PhiloxWarp>(I, C, variant == ACS_VARIANT_SPM_SEQ, s);
             else launch_spm_rng<Xoshiro>(I, C, variant == ACS_VARIANT_SPM_SEQ, s);
             break;
         default: break;
