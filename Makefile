@@ -21,7 +21,7 @@ CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -ffp-contract=off -I include \
             -I /usr/local/cuda/include
 
 CU_SRCS := $(SRC)/k_setup.cu $(SRC)/k_colony.cu $(SRC)/capi.cu
-CXX_SRCS := $(SRC)/instance.cpp $(SRC)/solver.cpp
+CXX_SRCS := $(SRC)/instance.cpp $(SRC)/solver.cpp $(SRC)/stats.cpp
 CU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS))
 CXX_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CXX_SRCS))
 HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard include/*.h) $(wildcard include/acs/*.hpp)

@@ -132,15 +132,19 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def ncu_traffic(variant: str):
-    """dram bytes per construct launch from the committed ncu --set full capture."""
+def ncu_record(variant: str) -> dict:
+    """The committed ncu --set full summary of this variant's construct kernel."""
     path = os.path.join(REPO, "profiles", "ncu_construct_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get(variant, {}).get("dram_bytes_per_launch")
+            return json.load(f).get(variant, {})
     except (OSError, ValueError):
-        return None
+        return {}
+
+
+def ncu_traffic(variant: str):
+    """dram bytes per construct launch from the committed ncu --set full capture."""
+    return ncu_record(variant).get("dram_bytes_per_launch")
 
 
 def cpu_baseline_seq(name: str, m: int, k: int):
@@ -288,6 +292,16 @@ def main():
                 "construct_ms_per_launch": round(construct_s * 1e3, 4),
                 "bytes_per_tour": B_tour,
                 "note": "latency-bound dependent-load chain; L2-resident working set"}
+    # the working set is L2-resident: the same bytes against the
+    # measured L2 read bandwidth, and the ncu L2 read traffic per launch
+    l2_gbs = P._native.l2_read_bandwidth(local, 48 << 20)
+    rec = ncu_record(args.variant)
+    sectors = rec.get("lts__t_sectors_srcunit_tex_op_read.sum")
+    roofline["l2"] = {"peak": round(l2_gbs, 1), "unit": "GB/s", "achieved": round(achieved, 1),
+                      "frac": round(achieved / l2_gbs, 4),
+                      "peak_source": "acs_gpu_l2_read_bandwidth: ld.global.cg stream over a 48 MiB "
+                                     "L2-resident buffer, measured in this run",
+                      "ncu_l2_read_bytes_per_launch": sectors * 32 if sectors else None}
 
     col.close()
     line = {

@@ -53,7 +53,7 @@ struct RunReport {
     std::vector<uint32_t> best_tour;
     int64_t best_length = 0;
     std::vector<int64_t> trace;      // L_gb after each iteration
-    std::vector<double> trace_ms;    // wall-clock at the end of each iteration chunk
+    std::vector<double> trace_ms;    // wall-clock ms of each iteration (interpolated inside a host chunk)
     std::optional<double> error_pct; // vs the instance optimum when known
     double total_ms = 0, setup_ms = 0, construct_ms_per_iter = 0;
     uint64_t iterations = 0, solutions = 0;

@@ -117,6 +117,15 @@ int acs_parse_tsplib(const char *text, size_t len, uint32_t *n, uint32_t *edge_w
  * reference RngStream(seed).uniform_int(side) (rng.hpp:16-84), x then y per node */
 int acs_random_instance(uint32_t n, uint64_t seed, uint32_t side, double *xs, double *ys);
 
+/* host-only: two-sided Wilcoxon rank-sum p-value (SPEC stats.rank_sum_test,
+ * SPEC.md:416-424): exact enumeration when nx + ny <= 12, else normal
+ * approximation with tie and continuity correction; nx, ny >= 3 */
+int acs_rank_sum_test(const double *xs, uint32_t nx, const double *ys, uint32_t ny, double *p);
+
+/* diagnostic: L2 read bandwidth (GB/s) streaming over an L2-resident buffer of
+ * `bytes` (the roofline denominator of the L2-resident construction working set) */
+int acs_gpu_l2_read_bandwidth(int device, uint64_t bytes, double *gbs);
+
 /* ---- stateless device ops (setup path) ----
  * replaces TspInstance ctor's dist_table_ (tsp_instance.cpp:23-47) */
 int acs_gpu_distance_table(const acs_instance_desc *inst, int device, int32_t *out /* n*n */);

@@ -68,6 +68,8 @@ SIGNATURES = {
     "acs_parse_tsplib": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(_u32), C.POINTER(_u32), _P, _P,
                                    _u32, C.c_char_p, C.c_size_t]),
     "acs_random_instance": (C.c_int, [_u32, _u64, _u32, _P, _P]),
+    "acs_gpu_l2_read_bandwidth": (C.c_int, [C.c_int, _u64, C.POINTER(_f64)]),
+    "acs_rank_sum_test": (C.c_int, [_P, _u32, _P, _u32, C.POINTER(_f64)]),
     "acs_gpu_distance_table": (C.c_int, [_desc, C.c_int, _P]),
     "acs_gpu_build_candidates": (C.c_int, [_desc, _u32, C.c_int, _P, C.POINTER(_u32)]),
     "acs_gpu_nn_tour_length": (C.c_int, [_desc, _u32, C.c_int, C.POINTER(_i64)]),
@@ -128,6 +130,13 @@ def check(rc: int, where: str) -> None:
         if rc == ACS_E_PARSE:
             raise ParseError(msg)
         raise AcsError(rc, where, msg)
+
+
+def l2_read_bandwidth(device: int = 0, nbytes: int = 64 << 20) -> float:
+    """Measured L2 read GB/s over an L2-resident buffer (roofline denominator)."""
+    g = C.c_double(0.0)
+    check(lib().acs_gpu_l2_read_bandwidth(device, nbytes, C.byref(g)), "l2_read_bandwidth")
+    return g.value
 
 
 def device_count() -> int:

@@ -172,6 +172,22 @@ def nn_tour_length(inst: TspInstance, start: int = 0, device: int = 0) -> int:
     return out.value
 
 
+def rank_sum_test(xs, ys) -> float:
+    """Two-sided Wilcoxon rank-sum p-value (SPEC stats.rank_sum_test)."""
+    a = np.ascontiguousarray(xs, np.float64)
+    b = np.ascontiguousarray(ys, np.float64)
+    p = C.c_double(0.0)
+    N.check(N.lib().acs_rank_sum_test(_ptr(a), len(a), _ptr(b), len(b), C.byref(p)), "rank_sum_test")
+    return p.value
+
+
+def relative_error(length: int, optimum: int) -> float:
+    """SPEC stats.relative_error."""
+    if optimum <= 0:
+        raise ValueError("relative_error: optimum must be > 0")
+    return 100.0 * (length - optimum) / optimum
+
+
 def default_q0(n: int) -> float:
     return 0.0 if n <= 20 else (n - 20) / n
 
@@ -336,12 +352,12 @@ def run(inst: TspInstance, params: AcsParams, device: int = 0) -> RunReport:
             if params.budget % m:
                 raise ValueError("budget must be a multiple of the ant count")
             iters = params.budget // m
-        trace, trace_ms, construct, done = [], [], 0.0, 0
+        trace, trace_ms, construct, done, chunk = [], [], 0.0, 0, 1
+        last = (time.perf_counter() - t0) * 1e3
         while True:
             if params.time_limit_s > 0:
                 if time.perf_counter() - t0 >= params.time_limit_s:
                     break
-                chunk = 8
             else:
                 if done >= iters:
                     break
@@ -349,8 +365,13 @@ def run(inst: TspInstance, params: AcsParams, device: int = 0) -> RunReport:
             st = col.iterate(chunk)
             construct += col.last_timing()[1]
             trace.extend(st["global_best_len"].tolist())
-            trace_ms.append((time.perf_counter() - t0) * 1e3)
-            done += chunk
+            now = (time.perf_counter() - t0) * 1e3
+            # per-iteration timestamps, interpolated inside a chunk
+            trace_ms.extend(last + (now - last) * (i + 1) / chunk for i in range(chunk))
+            if params.time_limit_s > 0:  # ~2 ms chunks: bounded overshoot, fine-grained trace
+                chunk = int(min(64, max(1, 2.0 * chunk / max(now - last, 1e-3))))
+            last = now
+            done += len(st)
         order, length = col.best()
         rep = RunReport(order, length, np.asarray(trace, np.int64), trace_ms,
                         None if inst.optimum is None else 100.0 * (length - inst.optimum) / inst.optimum,

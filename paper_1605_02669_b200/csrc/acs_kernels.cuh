@@ -92,6 +92,7 @@ void launch_ext_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, uin
                      double beta, int beta_int, uint64_t *scratch_keys, uint64_t *scratch_lower,
                      uint4 *ext, cudaStream_t s);
 void launch_fill(double *p, size_t count, double value, cudaStream_t s);
+void launch_l2_read(const uint4 *p, size_t count, uint32_t reps, uint32_t *sink, int sms, cudaStream_t s);
 void launch_spm_init(uint32_t *ids, double *vals, uint32_t *tail, uint32_t n, uint32_t S,
                      double tau_min, cudaStream_t s);
 void launch_rng_script(uint32_t kind, uint64_t seed, uint64_t it, uint64_t ant, int derive,

@@ -308,6 +308,41 @@ int acs_gpu_tour_lengths(const acs_instance_desc *inst, const uint32_t *routes, 
     return ACS_OK;
 }
 
+int acs_gpu_l2_read_bandwidth(int device, uint64_t bytes, double *gbs) {
+    if (!gbs || bytes < (1u << 20)) return fail(ACS_E_ARG, "null output or buffer below 1 MiB");
+    if (int rc = set_device(device)) return rc;
+    Stream st;
+    if (int rc = st.create()) return rc;
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const size_t count = bytes / sizeof(uint4);
+    DBuf<uint4> buf;
+    DBuf<uint32_t> sink;
+    CUDA_TRY(buf.alloc(count));
+    CUDA_TRY(sink.alloc(1));
+    CUDA_TRY(cudaMemsetAsync(buf.p, 1, buf.bytes(), st.s));
+    const uint32_t reps = 20;
+    launch_l2_read(buf.p, count, 2, sink.p, sms, st.s);  // warm: pull the buffer into L2
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int t = 0; t < 5; ++t) {
+        CUDA_TRY(cudaEventRecord(e0, st.s));
+        launch_l2_read(buf.p, count, reps, sink.p, sms, st.s);
+        CUDA_TRY(cudaEventRecord(e1, st.s));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        best = std::min(best, ms);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CUDA_TRY(cudaGetLastError());
+    *gbs = static_cast<double>(count) * sizeof(uint4) * reps / (best * 1e-3) / 1e9;
+    return ACS_OK;
+}
+
 int acs_gpu_rng_script(uint32_t kind, uint64_t seed, uint64_t iteration, uint64_t ant, int derive,
                        const int32_t *ops, const uint64_t *args, uint64_t *out, uint32_t count,
                        int device) {

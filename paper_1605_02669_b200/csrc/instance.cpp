@@ -173,16 +173,23 @@ TspInstance parse_tsplib(const std::string &text) {
     return parse_tsplib(in);
 }
 
-// plain or gzip-compressed TSPLIB file (zlib reads both transparently)
-TspInstance load_tsplib_file(const std::string &path) {
+namespace {
+// whole file, plain or gzip-compressed (zlib reads both transparently);
+// false when it cannot be opened or read
+bool read_maybe_gz(const std::string &path, std::string &text) {
     gzFile f = gzopen(path.c_str(), "rb");
-    if (!f) throw ParseError("cannot open instance file: " + path);
-    std::string text;
+    if (!f) return false;
     char buf[1 << 16];
     int got;
     while ((got = gzread(f, buf, sizeof(buf))) > 0) text.append(buf, static_cast<size_t>(got));
     gzclose(f);
-    if (got < 0) throw ParseError("cannot read instance file: " + path);
+    return got >= 0;
+}
+}  // namespace
+
+TspInstance load_tsplib_file(const std::string &path) {
+    std::string text;
+    if (!read_maybe_gz(path, text)) throw ParseError("cannot open instance file: " + path);
     return parse_tsplib(text);
 }
 
@@ -234,8 +241,9 @@ std::map<std::string, int64_t> load_optimum_catalog(std::istream &in) {
 }
 
 std::map<std::string, int64_t> load_optimum_catalog_file(const std::string &path) {
-    std::ifstream in(path);
-    if (!in.is_open()) throw std::runtime_error("cannot open optimum catalog: " + path);
+    std::string text;  // plain or .gz, like the instance files
+    if (!read_maybe_gz(path, text)) throw std::runtime_error("cannot open optimum catalog: " + path);
+    std::istringstream in(text);
     return load_optimum_catalog(in);
 }
 

@@ -32,6 +32,9 @@ def test_run_budget_forms(acs, gpu):
         acs.run(inst, acs.AcsParams(budget=199))
     r = acs.run(inst, acs.AcsParams(variant="spm", time_limit_s=0.3, seed=1))
     assert r.iterations >= 8 and r.hit_ratio() > 0.5
+    # one timestamp per iteration, increasing, ending near the limit (coarse check, D14)
+    assert len(r.trace_ms) == len(r.trace) == r.iterations
+    assert (np.diff(r.trace_ms) > 0).all() and 250 < r.trace_ms[-1] < 1500
 
 
 def test_cli_solve_csv(acs, gpu, tmp_path):
