@@ -204,3 +204,41 @@ def test_bench_product_path_does_not_use_the_oracle():
                 if isinstance(node, (ast.Import, ast.ImportFrom)):
                     mods = [a.name for a in node.names] if isinstance(node, ast.Import) else [node.module or ""]
                     assert not any(m.split(".")[0] == "oracle" for m in mods), fn.name
+
+
+CPP_STATS = r"""
+#include <cstdio>
+#include <vector>
+#include "acs/stats.hpp"
+#include "acs/solver.hpp"
+#include "acs/tsp_instance.hpp"
+int main() {
+    const std::vector<double> a{1, 2, 3}, b{4, 5, 6};
+    std::printf("%.6f %.6f\n", acs::rank_sum_test(a, b), acs::mann_whitney_u(a, b));
+    const std::vector<int64_t> len{2579, 2600, 2650};
+    const acs::SampleSummary s = acs::summarize(len, 2579);
+    std::printf("%.4f %.4f %lld %u\n", s.mean_error_pct, s.min_error_pct, (long long)s.best_length, s.runs);
+    const std::vector<double> good{1, 1.5, 2, 2.5, 3, 1.2, 1.1}, bad{5, 6, 7, 8, 9, 5.5, 6.5};
+    std::printf("%c%c\n", acs::significance_mark(good, bad), acs::significance_mark(bad, good));
+    const acs::TspInstance r = acs::random_uniform_instance(10000);
+    std::printf("%s %.0f %.0f %.2f\n", r.name_.c_str(), r.xs_[0], r.ys_[0], acs::relative_error(102, 100));
+    const auto cat = acs::load_optimum_catalog_file(ACS_CATALOG);
+    std::printf("%lld\n", (long long)cat.at("pr2392"));
+    return 0;
+}
+"""
+
+
+def test_cpp_stats_and_generators(acs, tmp_path):
+    src = tmp_path / "st.cpp"
+    src.write_text(CPP_STATS)
+    lib_dir = os.path.dirname(acs.LIB_PATH)
+    cat = os.path.join(REPO, "data", "tsplib", "optima.txt.gz")
+    subprocess.run(["/usr/bin/g++", "-std=c++20", f"-I{REPO}/include", f'-DACS_CATALOG="{cat}"', str(src),
+                    "-o", str(tmp_path / "st"), f"-L{lib_dir}", "-lacs_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+    out = subprocess.run([str(tmp_path / "st")], capture_output=True, text=True, check=True).stdout.split("\n")
+    assert out[0] == "0.100000 0.000000"
+    assert out[1] == f"{100 * (2609.6666666666665 - 2579) / 2579:.4f} 0.0000 2579 3"
+    assert out[2] == "+-"
+    assert out[3] == "rnd10k 120054 324231 2.00"
+    assert out[4] == "378032"
