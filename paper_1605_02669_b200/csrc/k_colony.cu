@@ -16,10 +16,14 @@
 #include <algorithm>
 #include <climits>
 
+#include <cooperative_groups.h>
+
 #include "../../include/acs_gpu.h"
 #include "acs_common.cuh"
 
 namespace acs_dev {
+
+namespace cg = cooperative_groups;
 
 struct Step {
     uint32_t v;        // chosen node
@@ -566,13 +570,6 @@ struct SpmRec {
             if (id[j] == v) hit = j;  // first (lowest) matching slot
         return hit;
     }
-    // slots holding v, as a bit mask
-    __device__ __forceinline__ uint32_t match(uint32_t v) const {
-        uint32_t m = 0;
-#pragma unroll
-        for (int j = 0; j < S; ++j) m |= (id[j] == v ? 1u : 0u) << j;
-        return m;
-    }
     // tau of (u, v) for this lane's v; all lanes must call (warp shuffle)
     __device__ __forceinline__ double lookup(uint32_t v, double tau_min) const {
         const int hit = find(v);
@@ -637,76 +634,23 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
         la.prepare(rng);
 
         for (uint32_t t = 1; t < n; ++t) {
-            // (1) the deferred half of edge (prev, cur) -- record cur gets
-            // neighbour prev (D4) -- and (2) the candidate lookups, computed
-            // side by side from the loaded record: a miss inserts prev at slot
-            // ts, evicting it, so lookups must not match ts.
-            const uint32_t ts = (rec.tail + 1) % S;
-            const uint32_t pm = rec.match(prev);
-            const bool pmiss = pending && pm == 0u;
-            const uint32_t c = el.x & kIdMask;
-            const uint32_t cm = rec.match(c) & (pmiss ? ~(1u << ts) : ~0u);
-            const int jc = cm ? __ffs(cm) - 1 : -1;
-            const double xv = __shfl_sync(kFull, rec.val, jc < 0 ? 0 : jc);
-            const double tau_lane = jc < 0 ? C.tau_min : xv;
-            if (pending) {  // apply (1) to the registers and write it through
-                const size_t base = static_cast<size_t>(cur) * S;
-                if (!pmiss) {
-                    const int ph = __ffs(pm) - 1;
-                    const double y = affine(__shfl_sync(kFull, rec.val, ph), C.c_l, C.c_0);
-                    if (lane == ph) rec.val = y;
-                    if (lane == 0) st_relaxed(C.spm_vals + base + ph, y);
-                    ++wc.hits;
-                } else {
-                    const double y = affine(C.tau_min, C.c_l, C.c_0);
-#pragma unroll
-                    for (int j = 0; j < S; ++j)
-                        if (j == static_cast<int>(ts)) rec.id[j] = prev;
-                    if (lane == static_cast<int>(ts)) rec.val = y;
-                    rec.tail = ts;
-                    if (lane == 0) {
-                        st_relaxed_u32(C.spm_ids + base + ts, prev);
-                        st_relaxed(C.spm_vals + base + ts, y);
-                        st_relaxed_u32(C.spm_tail + cur, ts);
-                    }
-                    ++wc.misses;
-                }
+            if (pending) {
+                if (rec.update(C, cur, prev, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
             }
+            const double tau_lane = rec.lookup(el.x & kIdMask, C.tau_min);
             Step st;
             select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
                         [&](uint32_t v, bool act) { return rec.lookup(act ? v : kEmpty, C.tau_min); }, st);
-            if (st.kind) wc.count(st.kind, n - t);
-            // slot of v in record cur (the lookups already found it for a
-            // candidate; the fallback searches), and cur's tail, before the
-            // registers are reused for record v
-            int jv = st.pos >= 0 ? __shfl_sync(kFull, jc, st.pos) : -1;
-            if (st.pos < 0) {
-                const uint32_t vm = rec.match(st.v);
-                jv = vm ? __ffs(vm) - 1 : -1;
-            }
-            const uint32_t tail_cur = rec.tail;
-            // next row and next record first, then the first half of edge (cur, v)
-            el = __ldg(C.rows + static_cast<size_t>(st.v) * 32 + lane);
-            rec.load(C, st.v, lane);
+            wc.count(st.kind, n - t);
+            el = __ldg(C.rows + static_cast<size_t>(st.v) * 32 + lane);  // next row first
             pending = (++kc == C.k);
             if (pending) {
                 kc = 0;
                 ++wc.updates;
-                const size_t base = static_cast<size_t>(cur) * S;
-                if (jv >= 0) {  // hit: tau_old is the record's value
-                    if (lane == 0) st_relaxed(C.spm_vals + base + jv, affine(st.tau_old, C.c_l, C.c_0));
-                    ++wc.hits;
-                } else {
-                    const uint32_t t2 = (tail_cur + 1) % S;
-                    if (lane == 0) {
-                        st_relaxed_u32(C.spm_ids + base + t2, st.v);
-                        st_relaxed(C.spm_vals + base + t2, affine(C.tau_min, C.c_l, C.c_0));
-                        st_relaxed_u32(C.spm_tail + cur, t2);
-                    }
-                    ++wc.misses;
-                }
+                if (rec.update(C, cur, st.v, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
                 prev = cur;
             }
+            rec.load(C, st.v, lane);  // record of the next node
             if (st.kind == 0) rng.advance();
             la.prepare(rng);
             vis[st.v >> 5] |= 1u << (st.v & 31);
@@ -737,42 +681,11 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
 
 // ============================================================ deferred (SYNC)
 
-// Software grid barrier for the cooperative (all-CTAs-resident) deferred kernel:
-// one arrival per CTA on bar[0]; the last arriver resets it and bumps the
-// generation bar[1] the others spin on.
-// Two-level: CTAs arrive on one of kBarGroups group counters (own 128 B line
-// each), the last of a group arrives on the root, the last root arriver bumps
-// the generation -- 8x fewer same-address atomics on the critical arrival path.
-constexpr unsigned kBarGroups = 8;
-__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned *gen = bar;
-        const unsigned g = *gen;
-        const unsigned grp = blockIdx.x % kBarGroups;
-        const unsigned members = nblocks / kBarGroups + (grp < nblocks % kBarGroups ? 1u : 0u);
-        const unsigned groups = nblocks < kBarGroups ? nblocks : kBarGroups;
-        unsigned *gcount = bar + 32 * (1 + grp);
-        unsigned *root = bar + 32 * (1 + kBarGroups);
-        __threadfence();
-        bool release = false;
-        if (atomicAdd(gcount, 1u) == members - 1) {
-            *gcount = 0;
-            if (atomicAdd(root, 1u) == groups - 1) {
-                *root = 0;
-                release = true;
-            }
-        }
-        if (release) {
-            __threadfence();
-            atomicAdd(bar, 1u);
-        } else {
-            while (*gen == g) __nanosleep(8);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
+// Grid-wide barrier of the cooperative (all-CTAs-resident) deferred kernel.
+// cooperative_groups' grid sync measured 1.3 us per barrier on B200 at
+// 148 x 640 threads, against 2.6 us for a two-level atomic-counter barrier
+// and 1.9 us for a flat acquire/release one (tools/micro/grid_barrier.cu).
+__device__ __forceinline__ void grid_sync(unsigned *, unsigned) { cg::this_grid().sync(); }
 
 template <class RNG>
 struct DefAnt {             // per-ant state of the deferred variant, in shared memory

@@ -12,6 +12,9 @@ $B sweep --instance $T/a280.tsp.gz --optima $CAT --variant spm --iterations 200 
 # 7: update period on nrw1379, m=256, 15 runs at k=1 and k=4 (relaxed, ACS-GPU-Alt)
 $B sweep --instance $T/nrw1379.tsp.gz --optima $CAT --variant relaxed --ants 256 --iterations 1000 \
   --reps 15 --sweep "k=1,4" --out gpurun_out/acc7_period > /dev/null
+# 7b: the same at m = n (the paper's Table freq-quality, where k=4 is significantly better at nrw1379)
+$B sweep --instance $T/nrw1379.tsp.gz --optima $CAT --variant relaxed --iterations 1000 \
+  --reps 15 --sweep "k=1,4" --out gpurun_out/acc7b_period_mn > /dev/null
 # 8: selective vs dense under equal wall-clock limits on a280, m=256, k=4, 15 runs each
 $B compare --instance $T/a280.tsp.gz --optima $CAT --ants 256 --update-period 4 --time-limit-ms 1000 \
   --reps 15 --a "memory=dense,consistent=0" --b "memory=selective" --out gpurun_out/acc8_compare > /dev/null
@@ -24,8 +27,9 @@ python - <<'PY'
 import json
 h = json.load(open("gpurun_out/acc6_hit_ratio.json"))
 print("acc6 hit ratio by s:", [(p["point"], round(sum(r["hit_ratio"] for r in p["reports"]) / len(p["reports"]), 4)) for p in h])
-k = json.load(open("gpurun_out/acc7_period.json"))
-print("acc7:", [(p["point"], p["mean_err_pct"], p["p_vs_baseline"], p["mark"]) for p in k])
+for f in ("acc7_period", "acc7b_period_mn"):
+    k = json.load(open(f"gpurun_out/{f}.json"))
+    print(f, [(p["point"], p["mean_err_pct"], p["p_vs_baseline"], p["mark"]) for p in k])
 c = json.load(open("gpurun_out/acc8_compare.json"))
 print("acc8: dense", c["A"]["mean_err_pct"], "selective", c["B"]["mean_err_pct"], "p", c["p_value"], "winner", c["winner"])
 s = json.loads(open("gpurun_out/acc9_seq.json").read().splitlines()[0])
