@@ -11,7 +11,10 @@ namespace acs_dev {
 
 
 constexpr int kBlock = 64;            // 2 ants per CTA: fine-grained spread over 148 SMs
-constexpr int kMaxRegs = 96;          // 5 warps per SM sub-partition (16K regs each): 20 ants per SM
+#ifndef ACS_MAXREGS
+#define ACS_MAXREGS 96
+#endif
+constexpr int kMaxRegs = ACS_MAXREGS;  // 96: 5 warps per SM sub-partition (16K regs each), 20 ants per SM
 constexpr int kWarpsPerBlock = kBlock / 32;
 constexpr int kDefBlock = 640;        // deferred persistent kernel: 20 warps, one CTA per SM
 constexpr uint32_t kIdMask = 0x00FFFFFFu;

@@ -376,8 +376,8 @@ __device__ __forceinline__ bool copy_index(uint32_t n, uint32_t u, uint32_t v, i
 //           `red.add` on a per-copy counter -- no update can be lost and no
 //           ant ever waits on an atomic -- and readers see f^c(base).  The
 //           iteration epilogue folds the counters back into the bases.
-template <int kMode, class RNG>
-__global__ void __maxnreg__(kMaxRegs) k_construct_dense(DevInstance I, DevColony C) {
+template <int kMode, class RNG, int kRegs = kMaxRegs>
+__global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C) {
     constexpr bool kAtomic = kMode == 1;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1038,6 +1038,31 @@ static void launch_tour_kernel(K kernel, const DevInstance &I, const DevColony &
     kernel<<<grid, threads, smem, s>>>(I, C);
 }
 
+// Register cap vs residency: at 96 registers 20 ants fit per SM (one wave for
+// pr2392); a colony larger than that runs in waves, and a 72-register build
+// (28 ants per SM, a few spills off the hot loop) finishes rnd10k in three
+// waves instead of four (measured: relaxed 41.9 -> 38.2, atomic 57.9 -> 49.8 ms).
+constexpr int kWideRegs = 72;
+
+template <int kMode, class RNG>
+static void launch_dense(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw = false) {
+    auto narrow = k_construct_dense<kMode, RNG, kMaxRegs>;
+    if (!one_warp) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const size_t smem = construct_smem(I, C, kBlock / 32, pw);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, narrow, kBlock, smem);
+        if (static_cast<uint64_t>(per_sm) * sms * (kBlock / 32) < C.m) {
+            launch_tour_kernel(k_construct_dense<kMode, RNG, kWideRegs>, I, C, false, s, pw);
+            return;
+        }
+    }
+    launch_tour_kernel(narrow, I, C, one_warp, s, pw);
+}
+
 template <class RNG>
 static void launch_spm_rng(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s) {
     switch (C.S) {
@@ -1054,16 +1079,16 @@ void launch_construct(int variant, int rng, const DevInstance &I, const DevColon
     const bool philox = rng == ACS_RNG_PHILOX;
     switch (variant) {
         case ACS_VARIANT_ATOMIC:
-            if (philox) launch_tour_kernel(k_construct_dense<1, PhiloxWarp>, I, C, false, s, true);
-            else launch_tour_kernel(k_construct_dense<1, Xoshiro>, I, C, false, s, true);
+            if (philox) launch_dense<1, PhiloxWarp>(I, C, false, s, true);
+            else launch_dense<1, Xoshiro>(I, C, false, s, true);
             break;
         case ACS_VARIANT_RELAXED:
-            if (philox) launch_tour_kernel(k_construct_dense<0, PhiloxWarp>, I, C, false, s);
-            else launch_tour_kernel(k_construct_dense<0, Xoshiro>, I, C, false, s);
+            if (philox) launch_dense<0, PhiloxWarp>(I, C, false, s);
+            else launch_dense<0, Xoshiro>(I, C, false, s);
             break;
         case ACS_VARIANT_SEQ:
-            if (philox) launch_tour_kernel(k_construct_dense<0, PhiloxWarp>, I, C, true, s);
-            else launch_tour_kernel(k_construct_dense<0, Xoshiro>, I, C, true, s);
+            if (philox) launch_dense<0, PhiloxWarp>(I, C, true, s);
+            else launch_dense<0, Xoshiro>(I, C, true, s);
             break;
         case ACS_VARIANT_SPM:
         case ACS_VARIANT_SPM_SEQ:

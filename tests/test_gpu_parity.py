@@ -183,3 +183,19 @@ def test_sync_more_ants_than_resident_warps(acs, orc, gpu):
     I = O.load("d198")
     r = pair(acs, orc, I, "sync", O.DENSE, m=3500, iters=2, seed=21)
     check_exact(*r, O.DENSE)
+
+
+@pytest.mark.parametrize("variant", ["atomic", "relaxed"])
+def test_colony_larger_than_one_wave(acs, orc, gpu, variant):
+    """m above the 96-register residency (20 ants per SM) launches the wide
+    (72-register) build; tours stay valid and the update count exact."""
+    I = O.load("d198")
+    m = 3500
+    with acs.Colony(to_acs(acs, I), acs.AcsParams(variant=variant, m=m, seed=8, rng="philox")) as col:
+        st = col.iterate(2)
+        routes, lens = col.routes()
+        cnt = col.counters()
+    assert_permutations(routes, I.n)
+    assert [int(lens[a]) for a in range(0, m, 97)] == [orc.tour_length(I, routes[a]) for a in range(0, m, 97)]
+    assert cnt["local_updates"] == 2 * m * I.n
+    assert st["iter_best_len"].tolist()[-1] == lens.min()
