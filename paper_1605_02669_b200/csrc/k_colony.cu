@@ -110,31 +110,88 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
     double bs = 0.0, bt = 0.0;
     uint32_t bv = 0xffffffffu;
     bool have = false;
-    constexpr int kChunks = 4;  // 4 x 32 nodes, 8 independent loads in flight per lane
-                                // (8 chunks spills at the 96-register occupancy cap)
-    for (uint32_t w = 0; w <= last; w += kChunks) {
-        uint32_t f[kChunks];
-        uint32_t any = 0;
+    if (erow) {
+        // With an eta^beta table (n <= 4096): coalesced 32-node chunks, four in
+        // flight, fully visited chunks skipped on the broadcast bitmask word.
+        constexpr int kChunks = 4;  // 8 independent loads per lane (8 chunks spill at the cap)
+        for (uint32_t w = 0; w <= last; w += kChunks) {
+            uint32_t f[kChunks];
+            uint32_t any = 0;
 #pragma unroll
-        for (int j = 0; j < kChunks; ++j) {
-            f[j] = (w + j <= last) ? ~vis[w + j] : 0u;
-            if (w + j == last) f[j] &= tail_mask;
-            any |= f[j];
+            for (int j = 0; j < kChunks; ++j) {
+                f[j] = (w + j <= last) ? ~vis[w + j] : 0u;
+                if (w + j == last) f[j] &= tail_mask;
+                any |= f[j];
+            }
+            if (any == 0u) continue;  // warp-uniform: all visited
+            double t[kChunks], e[kChunks];
+#pragma unroll
+            for (int j = 0; j < kChunks; ++j) {
+                const uint32_t v = (w + j) * 32 + lane;
+                const bool act = (f[j] >> lane) & 1u;
+                t[j] = tau_of(v, act);  // called by every lane (the SPM lookup shuffles)
+                e[j] = act ? __ldg(erow + v) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < kChunks; ++j) {
+                if ((f[j] >> lane) & 1u) {  // ascending v within the lane: strict > keeps the lowest id
+                    const double sc = __dmul_rn(t[j], e[j]);
+                    if (!have || sc > bs) { have = true; bs = sc; bv = (w + j) * 32 + lane; bt = t[j]; }
+                }
+            }
         }
-        if (any == 0u) continue;  // warp-uniform: all visited
-        double t[kChunks], e[kChunks];
-#pragma unroll
-        for (int j = 0; j < kChunks; ++j) {
-            const uint32_t v = (w + j) * 32 + lane;
-            const bool act = (f[j] >> lane) & 1u;
-            t[j] = tau_of(v, act);  // called by every lane (the SPM lookup shuffles)
-            e[j] = act ? eta_of(v) : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < kChunks; ++j) {
-            if ((f[j] >> lane) & 1u) {  // ascending v within the lane: strict > keeps the lowest id
-                const double s = __dmul_rn(t[j], e[j]);
-                if (!have || s > bs) { have = true; bs = s; bv = (w + j) * 32 + lane; bt = t[j]; }
+    } else {
+        // Without the table (n > 4096) eta^beta costs a sqrt and a pow per node, so
+        // only the unvisited ones are touched.  Compacted scan: the unvisited nodes of each group of 32 bitmask words are
+        // enumerated 32 per round, one per lane -- a warp prefix sum of the words'
+        // popcounts, a shuffle search for the owning word, __fns for the bit -- and
+        // the tau / eta^beta loads of 4 rounds are in flight together.  The cost
+        // follows the number of unvisited nodes, not n: late in a tour, where the
+        // pruned pass gives up, that is a few rounds instead of n/128 chunk loads.
+        constexpr int kRounds = 4;
+        for (uint32_t g = 0; g <= last; g += 32) {
+            const uint32_t w = g + lane;
+            uint32_t u = w <= last ? ~vis[w] : 0u;
+            if (w == last) u &= tail_mask;
+            const uint32_t pc = __popc(u);
+            uint32_t incl = pc;
+    #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const uint32_t total = __shfl_sync(kFull, incl, 31);
+            const uint32_t excl = incl - pc;
+            for (uint32_t b0 = 0; b0 < total; b0 += kRounds * 32) {
+                uint32_t vv[kRounds];
+                bool act[kRounds];
+                double t[kRounds], e[kRounds];
+    #pragma unroll
+                for (int r = 0; r < kRounds; ++r) {
+                    const uint32_t idx = b0 + r * 32 + lane;
+                    act[r] = idx < total;
+                    int src = 0;  // the last lane whose exclusive offset is <= idx owns it
+    #pragma unroll
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (__shfl_sync(kFull, excl, src + step) <= idx) src += step;
+                    const uint32_t ul = __shfl_sync(kFull, u, src);
+                    const uint32_t k = idx - __shfl_sync(kFull, excl, src);
+                    vv[r] = act[r] ? (g + src) * 32 + __fns(ul, 0, static_cast<int>(k) + 1) : 0u;
+                }
+    #pragma unroll
+                for (int r = 0; r < kRounds; ++r) {
+                    t[r] = tau_of(vv[r], act[r]);  // called by every lane (the SPM lookup shuffles)
+                    e[r] = act[r] ? eta_of(vv[r]) : 0.0;
+                }
+    #pragma unroll
+                for (int r = 0; r < kRounds; ++r) {
+                    if (act[r]) {
+                        const double sc = __dmul_rn(t[r], e[r]);
+                        if (!have || sc > bs || (sc == bs && vv[r] < bv)) {
+                            have = true; bs = sc; bv = vv[r]; bt = t[r];
+                        }
+                    }
+                }
             }
         }
     }
