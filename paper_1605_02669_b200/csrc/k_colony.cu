@@ -110,7 +110,10 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
     double bs = 0.0, bt = 0.0;
     uint32_t bv = 0xffffffffu;
     bool have = false;
-    if (erow) {
+#ifndef ACS_COMPACT_ALWAYS
+#define ACS_COMPACT_ALWAYS 0
+#endif
+    if (erow && !ACS_COMPACT_ALWAYS) {
         // With an eta^beta table (n <= 4096): coalesced 32-node chunks, four in
         // flight, fully visited chunks skipped on the broadcast bitmask word.
         constexpr int kChunks = 4;  // 8 independent loads per lane (8 chunks spill at the cap)
