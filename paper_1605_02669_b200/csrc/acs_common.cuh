@@ -45,32 +45,33 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t x, int m) {
 // hit -> in place, tail untouched; miss -> value from tau_min inserted at
 // (tail+1) % S evicting the least-recently inserted.  Relaxed accesses keep
 // the RELAXED contract's range invariants under races.
-__device__ __forceinline__ bool spm_update_mem(uint32_t *ids, double *vals, uint32_t *tail,
-                                               uint32_t S, uint32_t u, uint32_t v, double c_mul,
+// SPEC selective update of record u with neighbour v (D4-D6):
+// hit -> update in place, miss -> insert f(tau_min) at (tail+1) % S
+__device__ __forceinline__ bool spm_update_mem(const SpmMem &M, uint32_t u, uint32_t v, double c_mul,
                                                double c_add, double tau_min, double *stored) {
-    const size_t base = static_cast<size_t>(u) * S;
-    for (uint32_t j = 0; j < S; ++j) {
-        if (ld_relaxed_u32(ids + base + j) == v) {
-            const double y = affine(ld_relaxed(vals + base + j), c_mul, c_add);
-            st_relaxed(vals + base + j, y);
+    uint32_t *ids = M.ids(u);
+    double *vals = M.vals(u);
+    for (uint32_t j = 0; j < M.S; ++j) {
+        if (ld_relaxed_u32(ids + j) == v) {
+            const double y = affine(ld_relaxed(vals + j), c_mul, c_add);
+            st_relaxed(vals + j, y);
             if (stored) *stored = y;
             return true;
         }
     }
     const double y = affine(tau_min, c_mul, c_add);
-    const uint32_t t = (ld_relaxed_u32(tail + u) + 1) % S;
-    st_relaxed_u32(ids + base + t, v);
-    st_relaxed(vals + base + t, y);
-    st_relaxed_u32(tail + u, t);
+    const uint32_t t = (ld_relaxed_u32(M.tail(u)) + 1) % M.S;
+    st_relaxed_u32(ids + t, v);
+    st_relaxed(vals + t, y);
+    st_relaxed_u32(M.tail(u), t);
     if (stored) *stored = y;
     return false;
 }
 
-__device__ __forceinline__ double spm_read_mem(const uint32_t *ids, const double *vals, uint32_t S,
-                                               uint32_t u, uint32_t v, double tau_min) {
-    const size_t base = static_cast<size_t>(u) * S;
-    for (uint32_t j = 0; j < S; ++j)
-        if (ld_relaxed_u32(ids + base + j) == v) return ld_relaxed(vals + base + j);
+__device__ __forceinline__ double spm_read_mem(const SpmMem &M, uint32_t u, uint32_t v, double tau_min) {
+    const uint32_t *ids = M.ids(u);
+    for (uint32_t j = 0; j < M.S; ++j)
+        if (ld_relaxed_u32(ids + j) == v) return ld_relaxed(M.vals(u) + j);
     return tau_min;
 }
 

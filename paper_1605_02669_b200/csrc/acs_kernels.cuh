@@ -6,7 +6,7 @@
 //                         -- immutable, one coalesced 512 B row per step
 //   tauc   n x 32 f64     pheromone of the candidate edges, candidate order
 //   tau    n x n  f64     dense pheromone matrix (fallback + non-candidate edges)
-//   spm    n x S u32 ids, n x S f64 vals, n u32 tail  (selective memory)
+//   spm    n records {vals[S] f64 | ids[S] u32 | tail u32}, 128 B aligned (SpmMem)
 //   dist   n x n  i32     distance table (n <= 4096, as tsp_instance.hpp:31)
 //   routes m x n  u32, lens m i64
 #pragma once
@@ -15,6 +15,27 @@
 #include <cuda_runtime.h>
 
 namespace acs_dev {
+
+// Selective memory, record-major: record u is one 128 B-aligned block
+// {vals[S] f64 | ids[S] u32 | tail u32} (S = 8: 100 B in one line), so reading
+// a record is one line instead of three, and two records never share a line
+// (a store to record u never sits behind a pending load of record v).
+struct SpmMem {
+    unsigned char *base = nullptr;
+    uint32_t stride = 0;  // bytes per record, multiple of 128
+    uint32_t S = 0;
+    __host__ __device__ static uint32_t stride_for(uint32_t S) { return (12u * S + 4u + 127u) / 128u * 128u; }
+    __device__ __forceinline__ double *vals(uint32_t u) const {
+        return reinterpret_cast<double *>(base + static_cast<size_t>(u) * stride);
+    }
+    __device__ __forceinline__ uint32_t *ids(uint32_t u) const {
+        return reinterpret_cast<uint32_t *>(base + static_cast<size_t>(u) * stride + 8u * S);
+    }
+    __device__ __forceinline__ uint32_t *tail(uint32_t u) const {
+        return reinterpret_cast<uint32_t *>(base + static_cast<size_t>(u) * stride + 12u * S);
+    }
+};
+
 
 struct DevInstance {
     uint32_t n, words;   // words = ceil(n/32) visited-bitmask words
@@ -47,9 +68,7 @@ struct DevColony {
     const double *pw_lo;   // ATOMIC: c_l^j, j < 512
     const double *pw_hi;   // ATOMIC: c_l^(512 k), k < pw_hi_n
     uint32_t pw_hi_n;
-    uint32_t *spm_ids;     // n*S
-    double *spm_vals;      // n*S
-    uint32_t *spm_tail;    // n
+    SpmMem spm;            // selective memory (record-major), SPM variants only
     uint32_t *routes;      // m*n
     int64_t *lens;         // m
     unsigned long long *counters;  // [8], see Counter
@@ -93,14 +112,12 @@ void launch_ext_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, uin
                      uint4 *ext, cudaStream_t s);
 void launch_fill(double *p, size_t count, double value, cudaStream_t s);
 void launch_l2_read(const uint4 *p, size_t count, uint32_t reps, uint32_t *sink, int sms, cudaStream_t s);
-void launch_spm_init(uint32_t *ids, double *vals, uint32_t *tail, uint32_t n, uint32_t S,
-                     double tau_min, cudaStream_t s);
+void launch_spm_init(const SpmMem &M, uint32_t n, double tau_min, cudaStream_t s);
 void launch_rng_script(uint32_t kind, uint64_t seed, uint64_t it, uint64_t ant, int derive,
                        const int32_t *ops, const uint64_t *args, uint64_t *out, uint32_t count,
                        cudaStream_t s);
-void launch_spm_script(uint32_t *ids, double *vals, uint32_t *tail, uint32_t S, double tau_min,
-                       double c_l, double c_0, double alpha, double c_g, const uint32_t *ops,
-                       const int64_t *lgb, uint32_t count, double *out,
+void launch_spm_script(const SpmMem &M, double tau_min, double c_l, double c_0, double alpha, double c_g,
+                       const uint32_t *ops, const int64_t *lgb, uint32_t count, double *out,
                        unsigned long long *hits_misses, cudaStream_t s);
 
 // ---- per-iteration launchers ----

@@ -174,9 +174,11 @@ struct acs_gpu_ctx {
     DBuf<uint4> rows, ext;     // candidate rows; next-nearest rows for the pruned fallback
     DBuf<uint32_t> hot, hot_cnt;  // per-row non-candidate edges the global update touched
     DBuf<uint32_t> cand;  // flat n*L (reference layout), kept for get_candidates
-    DBuf<double> tau, tauc, spm_vals, etab, pw;
+    DBuf<double> tau, tauc, etab, pw;
+    DBuf<unsigned char> spm;   // record-major selective memory (SpmMem)
+    SpmMem spm_mem;
     DBuf<uint32_t> cnt, cntc;  // ATOMIC variant: pending local updates per copy
-    DBuf<uint32_t> spm_ids, spm_tail, routes, best_tour;
+    DBuf<uint32_t> routes, best_tour;
     DBuf<int64_t> lens, best_len;
     DBuf<uint64_t> iter;
     DBuf<unsigned long long> counters;
@@ -211,7 +213,7 @@ struct acs_gpu_ctx {
     }
     size_t device_bytes() const {
         return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + etab.bytes() + rows.bytes() + ext.bytes() + hot.bytes() + hot_cnt.bytes() + cand.bytes() +
-               tau.bytes() + tauc.bytes() + spm_vals.bytes() + spm_ids.bytes() + spm_tail.bytes() +
+               tau.bytes() + tauc.bytes() + spm.bytes() +
                routes.bytes() + best_tour.bytes() + lens.bytes() + cnt.bytes() + cntc.bytes();
     }
 };
@@ -366,6 +368,17 @@ int acs_gpu_rng_script(uint32_t kind, uint64_t seed, uint64_t iteration, uint64_
     return ACS_OK;
 }
 
+// record-major device image -> the ABI's separate n*S ids, n*S vals, n tails
+static void unpack_spm(const unsigned char *h, uint32_t stride, uint32_t S, uint32_t n, uint32_t *ids,
+                       double *vals, uint32_t *tail) {
+    for (uint32_t u = 0; u < n; ++u) {
+        const unsigned char *r = h + static_cast<size_t>(u) * stride;
+        if (vals) std::memcpy(vals + static_cast<size_t>(u) * S, r, 8u * S);
+        if (ids) std::memcpy(ids + static_cast<size_t>(u) * S, r + 8u * S, 4u * S);
+        if (tail) std::memcpy(tail + u, r + 12u * S, 4u);
+    }
+}
+
 int acs_gpu_spm_script(uint32_t n, uint32_t slots, double tau_min, double rho, double tau0,
                        double alpha, const uint32_t *ops, const int64_t *l_gb, uint32_t count,
                        int device, double *out, uint32_t *ids, double *vals, uint32_t *tail,
@@ -379,33 +392,33 @@ int acs_gpu_spm_script(uint32_t n, uint32_t slots, double tau_min, double rho, d
     if (int rc = set_device(device)) return rc;
     Stream st;
     if (int rc = st.create()) return rc;
-    DBuf<uint32_t> did, dtail, dops;
-    DBuf<double> dvals, dout;
+    DBuf<unsigned char> dspm;
+    DBuf<uint32_t> dops;
+    DBuf<double> dout;
     DBuf<int64_t> dl;
     DBuf<unsigned long long> hm;
-    CUDA_TRY(did.alloc(static_cast<size_t>(n) * slots));
-    CUDA_TRY(dvals.alloc(static_cast<size_t>(n) * slots));
-    CUDA_TRY(dtail.alloc(n));
+    const uint32_t stride = SpmMem::stride_for(slots);
+    CUDA_TRY(dspm.alloc(static_cast<size_t>(n) * stride));
+    const SpmMem M{dspm.p, stride, slots};
     CUDA_TRY(dops.alloc(3ull * count));
     CUDA_TRY(dout.alloc(count));
     CUDA_TRY(dl.alloc(count));
     CUDA_TRY(hm.alloc(2));
-    launch_spm_init(did.p, dvals.p, dtail.p, n, slots, tau_min, st.s);
+    launch_spm_init(M, n, tau_min, st.s);
     CUDA_TRY(cudaMemcpyAsync(dops.p, ops, dops.bytes(), cudaMemcpyHostToDevice, st.s));
     if (l_gb) CUDA_TRY(cudaMemcpyAsync(dl.p, l_gb, dl.bytes(), cudaMemcpyHostToDevice, st.s));
     else CUDA_TRY(cudaMemsetAsync(dl.p, 0, dl.bytes(), st.s));
     CUDA_TRY(cudaMemsetAsync(hm.p, 0, hm.bytes(), st.s));
     const double c_l = 1.0 - rho, c_0 = rho * tau0, c_g = 1.0 - alpha;
-    launch_spm_script(did.p, dvals.p, dtail.p, slots, tau_min, c_l, c_0, alpha, c_g, dops.p, dl.p,
-                      count, dout.p, hm.p, st.s);
+    launch_spm_script(M, tau_min, c_l, c_0, alpha, c_g, dops.p, dl.p, count, dout.p, hm.p, st.s);
     CUDA_TRY(cudaGetLastError());
     unsigned long long h[2] = {0, 0};
+    std::vector<unsigned char> img(dspm.bytes());
     if (out) CUDA_TRY(cudaMemcpyAsync(out, dout.p, dout.bytes(), cudaMemcpyDeviceToHost, st.s));
-    if (ids) CUDA_TRY(cudaMemcpyAsync(ids, did.p, did.bytes(), cudaMemcpyDeviceToHost, st.s));
-    if (vals) CUDA_TRY(cudaMemcpyAsync(vals, dvals.p, dvals.bytes(), cudaMemcpyDeviceToHost, st.s));
-    if (tail) CUDA_TRY(cudaMemcpyAsync(tail, dtail.p, dtail.bytes(), cudaMemcpyDeviceToHost, st.s));
+    CUDA_TRY(cudaMemcpyAsync(img.data(), dspm.p, img.size(), cudaMemcpyDeviceToHost, st.s));
     CUDA_TRY(cudaMemcpyAsync(h, hm.p, sizeof(h), cudaMemcpyDeviceToHost, st.s));
     CUDA_TRY(cudaStreamSynchronize(st.s));
+    unpack_spm(img.data(), stride, slots, n, ids, vals, tail);
     if (hits) *hits = h[0];
     if (misses) *misses = h[1];
     return ACS_OK;
@@ -510,10 +523,10 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
             CUDA_TRY(cudaStreamSynchronize(s));
         }
     } else {
-        CUDA_TRY(c->spm_ids.alloc(static_cast<size_t>(n) * c->S));
-        CUDA_TRY(c->spm_vals.alloc(static_cast<size_t>(n) * c->S));
-        CUDA_TRY(c->spm_tail.alloc(n));
-        launch_spm_init(c->spm_ids.p, c->spm_vals.p, c->spm_tail.p, n, c->S, c->tau0, s);
+        const uint32_t stride = SpmMem::stride_for(c->S);
+        CUDA_TRY(c->spm.alloc(static_cast<size_t>(n) * stride));
+        c->spm_mem = SpmMem{c->spm.p, stride, c->S};
+        launch_spm_init(c->spm_mem, n, c->tau0, s);
     }
     CUDA_TRY(c->routes.alloc(static_cast<size_t>(c->m) * n));
     CUDA_TRY(c->lens.alloc(c->m));
@@ -564,9 +577,7 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     C.pw_lo = c->pw.p;
     C.pw_hi = c->pw.p ? c->pw.p + 512 : nullptr;
     C.pw_hi_n = c->pw.p ? static_cast<uint32_t>(c->pw.count - 512) : 0;
-    C.spm_ids = c->spm_ids.p;
-    C.spm_vals = c->spm_vals.p;
-    C.spm_tail = c->spm_tail.p;
+    C.spm = c->spm_mem;
     C.routes = c->routes.p;
     C.lens = c->lens.p;
     C.counters = c->counters.p;
@@ -704,10 +715,10 @@ int acs_gpu_get_selective(const acs_gpu_ctx *c, uint32_t *ids, double *vals, uin
     if (c->dense()) return fail(ACS_E_ARG, "dense context has no selective memory");
     CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t s = c->stream.s;
-    if (ids) CUDA_TRY(cudaMemcpyAsync(ids, c->spm_ids.p, c->spm_ids.bytes(), cudaMemcpyDeviceToHost, s));
-    if (vals) CUDA_TRY(cudaMemcpyAsync(vals, c->spm_vals.p, c->spm_vals.bytes(), cudaMemcpyDeviceToHost, s));
-    if (tail) CUDA_TRY(cudaMemcpyAsync(tail, c->spm_tail.p, c->spm_tail.bytes(), cudaMemcpyDeviceToHost, s));
+    std::vector<unsigned char> h(c->spm.bytes());
+    CUDA_TRY(cudaMemcpyAsync(h.data(), c->spm.p, h.size(), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    unpack_spm(h.data(), c->spm_mem.stride, c->S, c->n, ids, vals, tail);
     return ACS_OK;
 }
 

@@ -609,19 +609,19 @@ struct SpmRec {
     uint32_t tail;
 
     __device__ __forceinline__ void load(const DevColony &C, uint32_t u, int lane) {
-        const size_t base = static_cast<size_t>(u) * S;
+        const uint32_t *ids = C.spm.ids(u);
         if constexpr (S >= 4) {
 #pragma unroll
             for (int j = 0; j < S; j += 4) {
-                const uint4 q = __ldcg(reinterpret_cast<const uint4 *>(C.spm_ids + base + j));
+                const uint4 q = __ldcg(reinterpret_cast<const uint4 *>(ids + j));
                 id[j] = q.x; id[j + 1] = q.y; id[j + 2] = q.z; id[j + 3] = q.w;
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < S; ++j) id[j] = __ldcg(C.spm_ids + base + j);
+            for (int j = 0; j < S; ++j) id[j] = __ldcg(ids + j);
         }
-        val = lane < S ? __ldcg(C.spm_vals + base + lane) : 0.0;
-        tail = __ldcg(C.spm_tail + u);
+        val = lane < S ? __ldcg(C.spm.vals(u) + lane) : 0.0;
+        tail = __ldcg(C.spm.tail(u));
     }
     __device__ __forceinline__ int find(uint32_t v) const {
         int hit = -1;
@@ -640,11 +640,10 @@ struct SpmRec {
     __device__ __forceinline__ bool update(const DevColony &C, uint32_t u, uint32_t v, double c_mul,
                                            double c_add, int lane) {
         const int hit = find(v);
-        const size_t base = static_cast<size_t>(u) * S;
         if (hit >= 0) {
             const double y = affine(__shfl_sync(kFull, val, hit), c_mul, c_add);
             if (lane == hit) val = y;
-            if (lane == 0) st_relaxed(C.spm_vals + base + hit, y);
+            if (lane == 0) st_relaxed(C.spm.vals(u) + hit, y);
             return true;
         }
         const double y = affine(C.tau_min, c_mul, c_add);
@@ -655,9 +654,9 @@ struct SpmRec {
         if (lane == static_cast<int>(t)) val = y;
         tail = t;
         if (lane == 0) {
-            st_relaxed_u32(C.spm_ids + base + t, v);
-            st_relaxed(C.spm_vals + base + t, y);
-            st_relaxed_u32(C.spm_tail + u, t);
+            st_relaxed_u32(C.spm.ids(u) + t, v);
+            st_relaxed(C.spm.vals(u) + t, y);
+            st_relaxed_u32(C.spm.tail(u), t);
         }
         return false;
     }
@@ -1033,8 +1032,8 @@ __global__ void k_global_spm(DevInstance I, DevColony C, DevBest B) {
         const uint32_t nb_next = B.tour[j + 1 == n ? 0 : j + 1];
         const uint32_t first = j == 0 ? nb_next : nb_prev;
         const uint32_t second = j == 0 ? nb_prev : nb_next;
-        if (spm_update_mem(C.spm_ids, C.spm_vals, C.spm_tail, C.S, r, first, B.c_g, c_d, C.tau_min, nullptr)) ++hits; else ++misses;
-        if (spm_update_mem(C.spm_ids, C.spm_vals, C.spm_tail, C.S, r, second, B.c_g, c_d, C.tau_min, nullptr)) ++hits; else ++misses;
+        if (spm_update_mem(C.spm, r, first, B.c_g, c_d, C.tau_min, nullptr)) ++hits; else ++misses;
+        if (spm_update_mem(C.spm, r, second, B.c_g, c_d, C.tau_min, nullptr)) ++hits; else ++misses;
         if (C.hot) {
             bool in1 = false, in2 = false;
             for (uint32_t l = 0; l < C.L; ++l) {

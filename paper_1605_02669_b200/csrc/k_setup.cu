@@ -224,13 +224,13 @@ __global__ void k_fill(double *p, size_t count, double v) {
         p[i] = v;
 }
 
-__global__ void k_spm_init(uint32_t *ids, double *vals, uint32_t *tail, uint32_t n, uint32_t S,
-                           double tau_min) {
+__global__ void k_spm_init(SpmMem M, uint32_t n, double tau_min) {
     for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-         i < static_cast<size_t>(n) * S; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        ids[i] = kEmpty;
-        vals[i] = tau_min;
-        if (i < n) tail[i] = S - 1;  // D5: first insertion lands in slot 0
+         i < static_cast<size_t>(n) * M.S; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const uint32_t u = static_cast<uint32_t>(i / M.S), j = static_cast<uint32_t>(i % M.S);
+        M.ids(u)[j] = kEmpty;
+        M.vals(u)[j] = tau_min;
+        if (j == 0) *M.tail(u) = M.S - 1;  // D5: first insertion lands in slot 0
     }
 }
 
@@ -269,14 +269,13 @@ __global__ void k_eta_table(DevInstance I, double beta, int beta_int, double *ou
     out[static_cast<size_t>(u) * I.n + v] = eta_beta(d, beta, beta_int);
 }
 
-__global__ void k_spm_script(uint32_t *ids, double *vals, uint32_t *tail, uint32_t S,
-                             double tau_min, double c_l, double c_0, double alpha, double c_g,
+__global__ void k_spm_script(SpmMem M, double tau_min, double c_l, double c_0, double alpha, double c_g,
                              const uint32_t *ops, const int64_t *lgb, uint32_t count, double *out,
                              unsigned long long *hm) {
     for (uint32_t i = 0; i < count; ++i) {
         const uint32_t u = ops[3 * i], v = ops[3 * i + 1], rule = ops[3 * i + 2];
         if (rule == 2) {
-            out[i] = spm_read_mem(ids, vals, S, u, v, tau_min);
+            out[i] = spm_read_mem(M, u, v, tau_min);
             continue;
         }
         double cm = c_l, ca = c_0;
@@ -284,7 +283,7 @@ __global__ void k_spm_script(uint32_t *ids, double *vals, uint32_t *tail, uint32
             cm = c_g;
             ca = __dmul_rn(alpha, __ddiv_rn(1.0, static_cast<double>(lgb[i])));
         }
-        const bool hit = spm_update_mem(ids, vals, tail, S, u, v, cm, ca, tau_min, &out[i]);
+        const bool hit = spm_update_mem(M, u, v, cm, ca, tau_min, &out[i]);
         hm[hit ? 0 : 1] += 1;
     }
 }
@@ -320,10 +319,9 @@ void launch_fill(double *p, size_t count, double value, cudaStream_t s) {
     k_fill<<<std::min<size_t>(blocks_for(count, 256), 148 * 16), 256, 0, s>>>(p, count, value);
 }
 
-void launch_spm_init(uint32_t *ids, double *vals, uint32_t *tail, uint32_t n, uint32_t S,
-                     double tau_min, cudaStream_t s) {
-    const size_t work = std::max<size_t>(static_cast<size_t>(n) * S, n);
-    k_spm_init<<<std::min<size_t>(blocks_for(work, 256), 148 * 16), 256, 0, s>>>(ids, vals, tail, n, S, tau_min);
+void launch_spm_init(const SpmMem &M, uint32_t n, double tau_min, cudaStream_t s) {
+    const size_t work = static_cast<size_t>(n) * M.S;
+    k_spm_init<<<std::min<size_t>(blocks_for(work, 256), 148 * 16), 256, 0, s>>>(M, n, tau_min);
 }
 
 void launch_rng_script(uint32_t kind, uint64_t seed, uint64_t it, uint64_t ant, int derive,
@@ -332,12 +330,10 @@ void launch_rng_script(uint32_t kind, uint64_t seed, uint64_t it, uint64_t ant, 
     k_rng_script<<<1, 1, 0, s>>>(kind, seed, it, ant, derive, ops, args, out, count);
 }
 
-void launch_spm_script(uint32_t *ids, double *vals, uint32_t *tail, uint32_t S, double tau_min,
-                       double c_l, double c_0, double alpha, double c_g, const uint32_t *ops,
-                       const int64_t *lgb, uint32_t count, double *out,
+void launch_spm_script(const SpmMem &M, double tau_min, double c_l, double c_0, double alpha, double c_g,
+                       const uint32_t *ops, const int64_t *lgb, uint32_t count, double *out,
                        unsigned long long *hits_misses, cudaStream_t s) {
-    k_spm_script<<<1, 1, 0, s>>>(ids, vals, tail, S, tau_min, c_l, c_0, alpha, c_g, ops, lgb,
-                                 count, out, hits_misses);
+    k_spm_script<<<1, 1, 0, s>>>(M, tau_min, c_l, c_0, alpha, c_g, ops, lgb, count, out, hits_misses);
 }
 
 void launch_ext_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, uint32_t ext_len,
