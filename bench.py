@@ -222,11 +222,20 @@ def main():
     import torch
     import paper_1605_02669_b200 as P
 
+    # one GPU per rank; if the ranks outnumber the visible GPUs (a test of the
+    # multi-rank path on one device) they share GPUs and exchange on the host
+    # over gloo (NCCL refuses two ranks on one device)
+    ndev = max(1, torch.cuda.device_count())
+    shared = world > ndev
+    local = local % ndev
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     inst = P.load_instance(args.instance)
     opt = inst.optimum
@@ -235,10 +244,15 @@ def main():
     seed = (args.seed + rank * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
     params = P.AcsParams(variant=args.variant, m=m, k=args.k, seed=seed, rng=rng_for(args.variant, args.rng))
     col = P.Colony(inst, params, device=local)
+    exchange = None
     if world > 1:
-        uid = [P.Colony.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        col.island_init(uid[0], world, rank)
+        if shared:
+            exchange = "host (gloo; ranks share a GPU)"
+        else:
+            uid = [P.Colony.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            col.island_init(uid[0], world, rank)
+            exchange = "device (NCCL inside libacs_b200)"
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     # our kernels per iteration: construction (1 launch; deferred = 1 cooperative
@@ -253,7 +267,10 @@ def main():
         ex = 0
         if world > 1 and (i + 1) % args.exchange_every == 0:
             t0 = time.perf_counter()
-            col.island_exchange()
+            if shared:
+                P.island.exchange_host(col, dist)
+            else:
+                col.island_exchange()
             ex = (time.perf_counter() - t0) * 1e3
         return tot + ex, con
 
@@ -272,7 +289,7 @@ def main():
     total_ms = sum(p[0] for p in per)
     construct_ms = sum(p[1] for p in per)
     if dist:
-        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cpu" if shared else f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     value = world * m * args.steps / (total_ms / 1e3)
@@ -317,7 +334,7 @@ def main():
                    "cl": 32, "k": args.k, "beta": 3.0, "alpha": 0.2, "rho": 0.01,
                    "q0": round(col.info.q0, 6), "rng": rng_for(args.variant, args.rng), "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": f"island x{world}" if world > 1 else "single colony",
-                   "exchange_every": args.exchange_every if world > 1 else None},
+                   "exchange_every": args.exchange_every if world > 1 else None, "exchange": exchange},
         "roofline": roofline,
         "gpu_launches": launches_per_iter * args.steps,
         "clocks": clk.summary(),
@@ -329,8 +346,10 @@ def main():
     }
     if rank == 0 and not args.no_variants:
         line["variants"] = other_variants(P, inst, args, local)
-    if rank == 0 and not args.no_e2e:
-        line["e2e"] = e2e(P, inst, params, args, world)
+    if not args.no_e2e:  # every rank: whole-job figure from the max wall time over ranks
+        e = e2e(P, inst, params, args, world, dist, local, shared)
+        if rank == 0:
+            line["e2e"] = e
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_seq(args.instance, m, args.k)
     if dist:
@@ -364,9 +383,11 @@ def other_variants(P, inst, args, device):
     return out
 
 
-def e2e(P, inst, params, args, world):
+def e2e(P, inst, params, args, world, dist=None, device=0, shared=False):
     """Same metric through the public one-call API (acs_gpu_run): host coords in,
-    host best tour + trace out, setup + K iterations inside the timed region."""
+    host best tour + trace out, setup + K iterations inside the timed region.
+    Every rank runs its own colony at the same time; the whole-job value uses
+    the max wall time over ranks."""
     import ctypes as C
     import numpy as np
     from paper_1605_02669_b200 import _native as N
@@ -377,15 +398,26 @@ def e2e(P, inst, params, args, world):
     trace = np.empty(K, np.int64)
     bl = C.c_int64()
     lib = N.lib()
+    # one untimed call first (lazy CUDA module loading of the setup kernels)
+    N.check(lib.acs_gpu_run(C.byref(d), C.byref(p), 1, device, order.ctypes.data_as(C.c_void_p), C.byref(bl),
+                            trace.ctypes.data_as(C.c_void_p)), "acs_gpu_run")
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
-    N.check(lib.acs_gpu_run(C.byref(d), C.byref(p), K, 0, order.ctypes.data_as(C.c_void_p), C.byref(bl),
+    N.check(lib.acs_gpu_run(C.byref(d), C.byref(p), K, device, order.ctypes.data_as(C.c_void_p), C.byref(bl),
                             trace.ctypes.data_as(C.c_void_p)), "acs_gpu_run")
     dt = time.perf_counter() - t0
+    if dist:
+        import torch
+        t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
     m = p.ants
-    return {"value": round(m * K / dt, 1), "unit": "tours/s",
+    return {"value": round(world * m * K / dt, 1), "unit": "tours/s",
             "h2d_bytes_per_step": round(2 * 8 * inst.n / K, 1),
             "d2h_bytes_per_step": round((4 * inst.n + 8) / K + 8, 1),
-            "api": "acs_gpu_run (create + K iterations + best tour/trace D2H + destroy), 1 GPU",
+            "api": f"acs_gpu_run (create + K iterations + best tour/trace D2H + destroy) on each of {world} "
+                   f"rank(s), max wall over ranks",
             "wall_s": round(dt, 4)}
 
 

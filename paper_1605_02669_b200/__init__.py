@@ -9,3 +9,4 @@ from .acs import (AcsError, AcsParams, CandidateLists, Colony, ParseError, RunRe
                   load_tsplib_file, nn_tour_length, optima, parse_tsplib, random_uniform_instance, rank_sum_test,
                   relative_error, run)
 from ._native import LIB_PATH, device_count, lib  # noqa: F401
+from . import island  # noqa: F401
