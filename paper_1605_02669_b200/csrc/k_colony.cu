@@ -605,6 +605,7 @@ __global__ void k_fold_counts(DevColony C, size_t dense_count, size_t cand_count
 template <int S>
 struct SpmRec {
     uint32_t id[S];
+    uint32_t idl;   // slot `lane`'s id (lanes < S, kEmpty above): warp-uniform finds are one ballot
     double val;     // slot `lane` (lanes < S)
     uint32_t tail;
 
@@ -621,7 +622,54 @@ struct SpmRec {
             for (int j = 0; j < S; ++j) id[j] = __ldcg(ids + j);
         }
         val = lane < S ? __ldcg(C.spm.vals(u) + lane) : 0.0;
+        idl = lane < S ? __ldcg(ids + lane) : kEmpty;
         tail = __ldcg(C.spm.tail(u));
+    }
+    // first slot holding the warp-uniform v, or -1
+    __device__ __forceinline__ int find_uniform(uint32_t v) const {
+        const unsigned m = __ballot_sync(kFull, idl == v);
+        return m ? __ffs(m) - 1 : -1;
+    }
+    // record u gets neighbour v (warp-uniform) with this record's registers kept
+    // current for later lookups in the same step; returns hit
+    __device__ __forceinline__ bool update_keep(const DevColony &C, uint32_t u, uint32_t v, double c_mul,
+                                                double c_add, int lane) {
+        const int hit = find_uniform(v);
+        if (hit >= 0) {
+            const double y = affine(__shfl_sync(kFull, val, hit), c_mul, c_add);
+            if (lane == hit) val = y;
+            if (lane == 0) st_relaxed(C.spm.vals(u) + hit, y);
+            return true;
+        }
+        const double y = affine(C.tau_min, c_mul, c_add);
+        const uint32_t t = (tail + 1) % S;
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+            if (j == static_cast<int>(t)) id[j] = v;
+        if (lane == static_cast<int>(t)) { idl = v; val = y; }
+        tail = t;
+        if (lane == 0) {
+            st_relaxed_u32(C.spm.ids(u) + t, v);
+            st_relaxed(C.spm.vals(u) + t, y);
+            st_relaxed_u32(C.spm.tail(u), t);
+        }
+        return false;
+    }
+    // the same, write-only: the registers are dead afterwards (next record loads)
+    __device__ __forceinline__ bool update_last(const DevColony &C, uint32_t u, uint32_t v, double tau_old,
+                                                double c_mul, double c_add, int lane) const {
+        const int hit = find_uniform(v);
+        if (hit >= 0) {
+            if (lane == 0) st_relaxed(C.spm.vals(u) + hit, affine(tau_old, c_mul, c_add));
+            return true;
+        }
+        const uint32_t t = (tail + 1) % S;
+        if (lane == 0) {
+            st_relaxed_u32(C.spm.ids(u) + t, v);
+            st_relaxed(C.spm.vals(u) + t, affine(C.tau_min, c_mul, c_add));
+            st_relaxed_u32(C.spm.tail(u), t);
+        }
+        return false;
     }
     __device__ __forceinline__ int find(uint32_t v) const {
         int hit = -1;
@@ -694,7 +742,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
 
         for (uint32_t t = 1; t < n; ++t) {
             if (pending) {
-                if (rec.update(C, cur, prev, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
+                if (rec.update_keep(C, cur, prev, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
             }
             const double tau_lane = rec.lookup(el.x & kIdMask, C.tau_min);
             Step st;
@@ -706,7 +754,9 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
             if (pending) {
                 kc = 0;
                 ++wc.updates;
-                if (rec.update(C, cur, st.v, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
+                // tau_old is what the selection read for (cur, v): the record's
+                // value on a hit
+                if (rec.update_last(C, cur, st.v, st.tau_old, C.c_l, C.c_0, lane)) ++wc.hits; else ++wc.misses;
                 prev = cur;
             }
             rec.load(C, st.v, lane);  // record of the next node
