@@ -55,10 +55,11 @@ clean:
 .PHONY: all oracle tools clean
 
 # A/B kernel experiments: make ab V=<name> DEFS="-DFOO=1" builds
-# paper_1605_02669_b200/libacs_b200_<name>.so (select with ACS_LIB_VARIANT=<name>)
+# paper_1605_02669_b200/libacs_b200_<name>.so (select with ACS_LIB_VARIANT=<name>);
+# COLONY=<file> builds another k_colony.cu (e.g. the previous commit's, as _ab_*.cu)
 ab:
 	@mkdir -p build/obj_$(V)
-	$(NVCC) $(NVFLAGS) $(DEFS) -c $(SRC)/k_colony.cu -o build/obj_$(V)/k_colony.o
+	$(NVCC) $(NVFLAGS) $(DEFS) -c $(or $(COLONY),$(SRC)/k_colony.cu) -o build/obj_$(V)/k_colony.o
 	$(NVCC) $(NVFLAGS) $(DEFS) -c $(SRC)/k_setup.cu -o build/obj_$(V)/k_setup.o
 	$(NVCC) $(NVFLAGS) $(DEFS) -c $(SRC)/capi.cu -o build/obj_$(V)/capi.o
 	$(NVCC) $(ARCH) -shared -o $(PKG)/libacs_b200_$(V).so build/obj_$(V)/k_colony.o build/obj_$(V)/k_setup.o \

@@ -34,71 +34,23 @@ struct Step {
     int kind;          // 0 greedy, 1 roulette, 2 fallback
 };
 
-// Full-scan fallback (Alg.2 l.18): argmax tau*eta^beta over all
-// unvisited nodes, ties -> lowest id, no RNG draw (P1).  Lane l of chunk w
-// evaluates node 32w+l, so pheromone-row and eta-row reads are coalesced
-// 256 B transactions; fully visited chunks are skipped on the (broadcast)
-// bitmask word and two chunks are in flight per iteration.
+// Per-lane running best of a full-scan fallback (score, node, trail value).
+struct ScanBest {
+    double bs = 0.0, bt = 0.0;
+    uint32_t bv = 0xffffffffu;
+    bool have = false;
+};
+
+// Full scan (Alg.2 l.18) of the unvisited nodes in bitmask words
+// [wb, we): per-lane argmax of tau*eta^beta, nodes ascending within a lane, so
+// a strict > keeps the lowest id.  The whole fallback is this over [0, words)
+// followed by finish_scan; the deferred kernel splits the range over the warps
+// of a CTA and combines the per-warp results (argmax, ties -> lowest id).
 template <class TauFn>
-__device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevColony &C,
-                                              const uint32_t *vis, uint32_t cur, TauFn tau_of,
-                                              int lane, Step &o) {
+__device__ __forceinline__ void full_scan_range(const DevInstance &I, const DevColony &C,
+                                                const uint32_t *vis, uint32_t cur, TauFn tau_of, int lane,
+                                                uint32_t wb, uint32_t we, ScanBest &b) {
     const double xc = __ldg(I.xs + cur), yc = __ldg(I.ys + cur);
-    // Exact pruned pass.  Only the global update raises a trail above tau0
-    // (local updates move it towards tau0), and every non-candidate edge it
-    // ever touched is in cur's hot list.  So: score the hot list exactly, then
-    // walk the next-nearest neighbours in distance order; once
-    // tau_bound * eta^beta(last scanned) < best, no unscanned node can win or
-    // tie, and the result equals the full scan's (argmax, ties -> lowest id).
-    const uint32_t hcnt = C.ext_len ? __ldg(C.hot_cnt + cur) : kHot + 1;
-    if (hcnt <= kHot) {
-        double bs = 0.0, bt = 0.0;
-        uint32_t bv = 0xffffffffu;
-        bool have = false;
-        {
-            const bool in_list = static_cast<uint32_t>(lane) < hcnt;
-            const uint32_t v = in_list ? __ldg(C.hot + static_cast<size_t>(cur) * kHot + lane) : 0u;
-            const bool act = in_list && !visited(vis, v);
-            const double tv = tau_of(v, act);
-            if (act) {
-                const double e = I.etab ? __ldg(I.etab + static_cast<size_t>(cur) * I.n + v)
-                                        : eta_beta(tsplib_distance(I.type, xc, yc, __ldg(I.xs + v), __ldg(I.ys + v)),
-                                                   C.beta, C.beta_int);
-                have = true; bs = __dmul_rn(tv, e); bv = v; bt = tv;
-            }
-        }
-        const uint4 *xrow = C.ext + static_cast<size_t>(cur) * C.ext_len;
-        for (uint32_t base = 0; base < C.ext_len; base += 32) {
-            const uint4 q = __ldg(xrow + base + lane);
-            const bool in_list = q.x != kEmpty;
-            const bool act = in_list && !visited(vis, q.x);
-            const double tv = tau_of(in_list ? q.x : 0u, act);
-            if (act) {
-                const double sc = __dmul_rn(tv, __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z)));
-                if (!have || sc > bs || (sc == bs && q.x < bv)) { have = true; bs = sc; bv = q.x; bt = tv; }
-            }
-            double sb = bs;
-            uint32_t node = have ? bv : 0xffffffffu;
-            warp_argmax_node(sb, node, have);
-            // the list ends inside this slice: every non-candidate node was scanned
-            const bool exhausted = __any_sync(kFull, !in_list);
-            const uint32_t lw = __shfl_sync(kFull, q.w, 31), lz = __shfl_sync(kFull, q.z, 31);
-            const double bound = __dmul_rn(C.tau_bound, __hiloint2double(static_cast<int>(lw), static_cast<int>(lz)));
-            if (node != 0xffffffffu && (exhausted || bound < sb)) {
-                const unsigned owner = __ballot_sync(kFull, have && bv == node);
-                o.v = node;
-                o.tau_old = __shfl_sync(kFull, bt, __ffs(owner) - 1);
-                o.d = tsplib_distance(I.type, xc, yc, __ldg(I.xs + node), __ldg(I.ys + node));
-                o.pos = -1;
-                o.kind = 2;
-                const uint32_t id = __ldg(&C.rows[static_cast<size_t>(node) * 32 + lane].x) & kIdMask;
-                const unsigned mm = __ballot_sync(kFull, static_cast<uint32_t>(lane) < C.L && id == cur);
-                o.mirror = mm ? static_cast<uint32_t>(__ffs(mm) - 1) : kNoMirror;
-                return;
-            }
-        }
-    }
-    if (lane == 0) atomicAdd(C.counters + kCntFallbackFull, 1ull);
     const double *erow = I.etab ? I.etab + static_cast<size_t>(cur) * I.n : nullptr;
     auto eta_of = [&](uint32_t v) -> double {
         if (erow) return __ldg(erow + v);
@@ -107,9 +59,6 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
     };
     const uint32_t last = I.words - 1;
     const uint32_t tail_mask = (I.n & 31) ? ((1u << (I.n & 31)) - 1u) : 0xffffffffu;
-    double bs = 0.0, bt = 0.0;
-    uint32_t bv = 0xffffffffu;
-    bool have = false;
 #ifndef ACS_COMPACT_ALWAYS
 #define ACS_COMPACT_ALWAYS 0
 #endif
@@ -117,12 +66,12 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
         // With an eta^beta table (n <= 4096): coalesced 32-node chunks, four in
         // flight, fully visited chunks skipped on the broadcast bitmask word.
         constexpr int kChunks = 4;  // 8 independent loads per lane (8 chunks spill at the cap)
-        for (uint32_t w = 0; w <= last; w += kChunks) {
+        for (uint32_t w = wb; w < we; w += kChunks) {
             uint32_t f[kChunks];
             uint32_t any = 0;
 #pragma unroll
             for (int j = 0; j < kChunks; ++j) {
-                f[j] = (w + j <= last) ? ~vis[w + j] : 0u;
+                f[j] = (w + j < we) ? ~vis[w + j] : 0u;
                 if (w + j == last) f[j] &= tail_mask;
                 any |= f[j];
             }
@@ -139,7 +88,7 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
             for (int j = 0; j < kChunks; ++j) {
                 if ((f[j] >> lane) & 1u) {  // ascending v within the lane: strict > keeps the lowest id
                     const double sc = __dmul_rn(t[j], e[j]);
-                    if (!have || sc > bs) { have = true; bs = sc; bv = (w + j) * 32 + lane; bt = t[j]; }
+                    if (!b.have || sc > b.bs) { b.have = true; b.bs = sc; b.bv = (w + j) * 32 + lane; b.bt = t[j]; }
                 }
             }
         }
@@ -152,9 +101,9 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
         // follows the number of unvisited nodes, not n: late in a tour, where the
         // pruned pass gives up, that is a few rounds instead of n/128 chunk loads.
         constexpr int kRounds = 4;
-        for (uint32_t g = 0; g <= last; g += 32) {
+        for (uint32_t g = wb; g < we; g += 32) {
             const uint32_t w = g + lane;
-            uint32_t u = w <= last ? ~vis[w] : 0u;
+            uint32_t u = w < we ? ~vis[w] : 0u;
             if (w == last) u &= tail_mask;
             const uint32_t pc = __popc(u);
             uint32_t incl = pc;
@@ -190,27 +139,103 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
                 for (int r = 0; r < kRounds; ++r) {
                     if (act[r]) {
                         const double sc = __dmul_rn(t[r], e[r]);
-                        if (!have || sc > bs || (sc == bs && vv[r] < bv)) {
-                            have = true; bs = sc; bv = vv[r]; bt = t[r];
+                        if (!b.have || sc > b.bs || (sc == b.bs && vv[r] < b.bv)) {
+                            b.have = true; b.bs = sc; b.bv = vv[r]; b.bt = t[r];
                         }
                     }
                 }
             }
         }
     }
-    double s = bs;
-    uint32_t node = have ? bv : 0xffffffffu;
-    warp_argmax_node(s, node, have);
-    const unsigned owner = __ballot_sync(kFull, have && bv == node);
+}
+
+// The fallback's chosen node `node` (warp-uniform) with its trail value:
+// distance and the mirror slot (where cur sits in node's candidate row).
+__device__ __forceinline__ void finish_scan(const DevInstance &I, const DevColony &C, uint32_t cur,
+                                            uint32_t node, double tau_old, int lane, Step &o) {
     o.v = node;
-    o.tau_old = __shfl_sync(kFull, bt, __ffs(owner) - 1);
-    o.d = tsplib_distance(I.type, xc, yc, __ldg(I.xs + node), __ldg(I.ys + node));
+    o.tau_old = tau_old;
+    o.d = tsplib_distance(I.type, __ldg(I.xs + cur), __ldg(I.ys + cur), __ldg(I.xs + node), __ldg(I.ys + node));
     o.pos = -1;
     o.kind = 2;
-    // mirror: where does cur sit in v's candidate row?
     const uint32_t id = __ldg(&C.rows[static_cast<size_t>(node) * 32 + lane].x) & kIdMask;
     const unsigned mm = __ballot_sync(kFull, static_cast<uint32_t>(lane) < C.L && id == cur);
     o.mirror = mm ? static_cast<uint32_t>(__ffs(mm) - 1) : kNoMirror;
+}
+
+// Fallback (Alg.2 l.18): argmax tau*eta^beta over all unvisited
+// nodes, ties -> lowest id, no RNG draw (P1).  An exact pruned pass first; if
+// it cannot decide, the full scan -- or, with kDefer (the deferred kernel),
+// o.kind = 3: the caller's CTA runs the full scan cooperatively.
+template <bool kDefer = false, class TauFn>
+__device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevColony &C,
+                                              const uint32_t *vis, uint32_t cur, TauFn tau_of,
+                                              int lane, Step &o) {
+    const double xc = __ldg(I.xs + cur), yc = __ldg(I.ys + cur);
+    // Exact pruned pass.  Only the global update raises a trail above tau0
+    // (local updates move it towards tau0), and every non-candidate edge it
+    // ever touched is in cur's hot list.  So: score the hot list exactly, then
+    // walk the next-nearest neighbours in distance order; once
+    // tau_bound * eta^beta(last scanned) < best, no unscanned node can win or
+    // tie, and the result equals the full scan's (argmax, ties -> lowest id).
+    // The hot count, the hot list and the first next-nearest slice are
+    // independent loads: issued together, so the common case (decided in the
+    // first slice) costs two dependent L2 trips (ids, then trails) instead of five.
+    const uint32_t hcnt = C.ext_len ? __ldg(C.hot_cnt + cur) : kHot + 1;
+    const uint32_t hv = C.ext_len ? __ldg(C.hot + static_cast<size_t>(cur) * kHot + lane) : 0u;
+    const uint4 *xrow = C.ext + static_cast<size_t>(cur) * C.ext_len;
+    uint4 q = C.ext_len ? __ldg(xrow + lane) : make_uint4(kEmpty, 0u, 0u, 0u);
+    if (hcnt <= kHot) {
+        double bs = 0.0, bt = 0.0;
+        uint32_t bv = 0xffffffffu;
+        bool have = false;
+        {
+            const bool in_list = static_cast<uint32_t>(lane) < hcnt;
+            const uint32_t v = in_list ? hv : 0u;
+            const bool act = in_list && !visited(vis, v);
+            const double tv = tau_of(v, act);
+            if (act) {
+                const double e = I.etab ? __ldg(I.etab + static_cast<size_t>(cur) * I.n + v)
+                                        : eta_beta(tsplib_distance(I.type, xc, yc, __ldg(I.xs + v), __ldg(I.ys + v)),
+                                                   C.beta, C.beta_int);
+                have = true; bs = __dmul_rn(tv, e); bv = v; bt = tv;
+            }
+        }
+        for (uint32_t base = 0; base < C.ext_len; base += 32) {
+            if (base) q = __ldg(xrow + base + lane);
+            const bool in_list = q.x != kEmpty;
+            const bool act = in_list && !visited(vis, q.x);
+            const double tv = tau_of(in_list ? q.x : 0u, act);
+            if (act) {
+                const double sc = __dmul_rn(tv, __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z)));
+                if (!have || sc > bs || (sc == bs && q.x < bv)) { have = true; bs = sc; bv = q.x; bt = tv; }
+            }
+            double sb = bs;
+            uint32_t node = have ? bv : 0xffffffffu;
+            warp_argmax_node(sb, node, have);
+            // the list ends inside this slice: every non-candidate node was scanned
+            const bool exhausted = __any_sync(kFull, !in_list);
+            const uint32_t lw = __shfl_sync(kFull, q.w, 31), lz = __shfl_sync(kFull, q.z, 31);
+            const double bound = __dmul_rn(C.tau_bound, __hiloint2double(static_cast<int>(lw), static_cast<int>(lz)));
+            if (node != 0xffffffffu && (exhausted || bound < sb)) {
+                const unsigned owner = __ballot_sync(kFull, have && bv == node);
+                finish_scan(I, C, cur, node, __shfl_sync(kFull, bt, __ffs(owner) - 1), lane, o);
+                return;
+            }
+        }
+    }
+    if (lane == 0) atomicAdd(C.counters + kCntFallbackFull, 1ull);
+    if constexpr (kDefer) {
+        o.kind = 3;
+        return;
+    }
+    ScanBest b;
+    full_scan_range(I, C, vis, cur, tau_of, lane, 0u, I.words, b);
+    double s = b.bs;
+    uint32_t node = b.have ? b.bv : 0xffffffffu;
+    warp_argmax_node(s, node, b.have);
+    const unsigned owner = __ballot_sync(kFull, b.have && b.bv == node);
+    finish_scan(I, C, cur, node, __shfl_sync(kFull, b.bt, __ffs(owner) - 1), lane, o);
 }
 
 // The q draw of the next step, computed speculatively on a copy of the stream
@@ -290,7 +315,7 @@ __device__ __forceinline__ void rng_init(PhiloxWarp &rng, const DevColony &C, ui
 // Stream commit: roulette commits q (and draws r) here; for a greedy step
 // (o.kind == 0) the caller commits q with rng.advance() AFTER issuing the next
 // row load, which keeps the state transition off the dependent chain.
-template <class RNG, class TauFn>
+template <bool kDefer = false, class RNG, class TauFn>
 __device__ __forceinline__ void select_step(const DevInstance &I, const DevColony &C,
                                             const uint32_t *vis, uint32_t cur, uint4 el,
                                             double tau_lane, RNG &rng, const Lookahead<RNG> &la,
@@ -319,7 +344,7 @@ __device__ __forceinline__ void select_step(const DevInstance &I, const DevColon
         o.tau_old = __shfl_sync(kFull, tau_lane, pos);
         return;
     }
-    fallback_scan(I, C, vis, cur, tau_of, lane, o);
+    fallback_scan<kDefer>(I, C, vis, cur, tau_of, lane, o);
 }
 
 // Per-ant event counters, 32-bit (one tour has < n^2/2 fallback elements and
@@ -801,6 +826,28 @@ struct DefAnt {             // per-ant state of the deferred variant, in shared 
     RNG rng;
     long long len;
     uint32_t cur, start, v, slots;  // slots = pos | mirror << 8 of this step's edge
+    int32_t d;                      // distance of this step's edge
+    int kind;                       // 0 greedy, 1 roulette, 2 fallback, 3 full scan requested
+};
+
+// One warp's share of a cooperative full scan: (score, node, trail) of its
+// word range, combined by the requesting warp (argmax, ties -> lowest id).
+struct ScanPart {
+    double s, t;
+    uint32_t v;
+};
+
+// Shared-memory layout of the deferred kernel (wpb warps, A ants per warp).
+struct DefSmem {
+    size_t ants_off, vis_off, part_off, req_off, bytes;
+    __host__ __device__ DefSmem(uint32_t wpb, uint32_t A, uint32_t words) {
+        ants_off = static_cast<size_t>(wpb) * 32 * sizeof(double);  // roulette scratch
+        vis_off = ants_off + static_cast<size_t>(wpb) * A * 64;      // DefAnt <= 64 B
+        part_off = vis_off + static_cast<size_t>(wpb) * A * words * sizeof(uint32_t);
+        part_off = (part_off + 15) & ~static_cast<size_t>(15);
+        req_off = part_off + static_cast<size_t>(wpb) * A * wpb * sizeof(ScanPart);
+        bytes = req_off + (static_cast<size_t>(wpb) * A + 1) * sizeof(uint32_t);
+    }
 };
 
 // Fold the pending count of one copy into its base by applying f c times in
@@ -813,10 +860,12 @@ __device__ __forceinline__ void fold_copy(const DevColony &C, uint32_t n, uint32
     const int pos = (slots & 0xFFu) == 0xFFu ? -1 : static_cast<int>(slots & 0xFFu);
     if (!copy_index(n, u, v, pos, (slots >> 8) & 0xFFu, lane, dense, k)) return;
     uint32_t *cp = (dense ? C.cnt : C.cntc) + k;
+    double *bp = (dense ? C.tau : C.tauc) + k;
+    // the base is loaded alongside the exchange: only the ant that receives
+    // the count writes it, so the value read here is current for that ant
+    double x = ld_relaxed(bp);
     const uint32_t c = atomicExch(cp, 0u);
     if (c) {
-        double *bp = (dense ? C.tau : C.tauc) + k;
-        double x = ld_relaxed(bp);
         for (uint32_t i = 0; i < c; ++i) x = affine(x, C.c_l, C.c_0);
         st_relaxed(bp, x);
     }
@@ -838,23 +887,39 @@ __device__ __forceinline__ void bump_copy(const DevColony &C, uint32_t n, uint32
 // applies f that many times; grid barrier.  The affine updates commute, so the
 // result is bit-identical to the oracle's ant-ordered application.  Closing
 // edges are a separate pass after step n-1 (PAPER Alg.1 l.13-14).
+//
+// The lockstep makes a step as slow as its slowest ant, and the slowest ant is
+// one whose fallback the pruned pass could not decide: a full scan of n nodes.
+// Those scans are not run by the one warp: an ant that needs one posts a
+// request, and ALL warps of the CTA (idle until the grid barrier otherwise)
+// scan a slice of its bitmask words each; the requester combines the slices.
 template <class RNG>
 __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, DevDeferred D) {
+    static_assert(sizeof(DefAnt<RNG>) <= 64, "DefSmem reserves 64 B per ant");
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     const uint32_t A = D.ants_per_warp;
     const uint32_t W = gridDim.x * wpb;
-    const uint32_t gw = blockIdx.x * wpb + wib;
+    // warp-major across CTAs: ant a runs in CTA a % grid, so a colony smaller
+    // than the resident warps spreads evenly over every SM
+    const uint32_t gw = wib * gridDim.x + blockIdx.x;
     const uint32_t n = I.n;
+    const DefSmem L(wpb, A, I.words);
     double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
-    DefAnt<RNG> *ants = reinterpret_cast<DefAnt<RNG> *>(smem + wpb * 32 * sizeof(double)) + wib * A;
-    uint32_t *vis_base = reinterpret_cast<uint32_t *>(smem + wpb * 32 * sizeof(double) +
-                                                      wpb * A * sizeof(DefAnt<RNG>)) +
-                         static_cast<size_t>(wib) * A * I.words;
+    DefAnt<RNG> *ants_cta = reinterpret_cast<DefAnt<RNG> *>(smem + L.ants_off);
+    DefAnt<RNG> *ants = ants_cta + wib * A;
+    uint32_t *vis_cta = reinterpret_cast<uint32_t *>(smem + L.vis_off);
+    uint32_t *vis_base = vis_cta + static_cast<size_t>(wib) * A * I.words;
+    ScanPart *parts = reinterpret_cast<ScanPart *>(smem + L.part_off);  // [request][warp]
+    uint32_t *nreq = reinterpret_cast<uint32_t *>(smem + L.req_off);
+    uint32_t *reqs = nreq + 1;                                            // (warp << 16) | ant slot
+    // slice of the bitmask words per warp in a cooperative scan (multiple of 4)
+    const uint32_t slice = ((I.words + wpb - 1) / wpb + 3) & ~3u;
     const uint64_t it = *C.iter;
     WarpCounters wc;
     uint32_t my_ants = 0;
+    if (threadIdx.x == 0) *nreq = 0;
 
     for (uint32_t j = 0; j < A; ++j) {
         const uint32_t a = gw + j * W;
@@ -880,8 +945,8 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
 
     for (uint32_t t = 1; t < n; ++t) {
         const bool due = (t % C.k) == 0;
+        // (1) selection against the step-start pheromone; undecided fallbacks post a request
         for (uint32_t j = 0; j < my_ants; ++j) {
-            const uint32_t a = gw + j * W;
             uint32_t *vis = vis_base + j * I.words;
             DefAnt<RNG> &s = ants[j];
             const uint32_t cur = s.cur;
@@ -892,26 +957,92 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
             Lookahead<RNG> la;
             la.prepare(rng);
             Step st;
-            select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
-                        [&](uint32_t v, bool act) {
-                            return act ? ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v) : 0.0;
-                        },
-                        st);
+            select_step<true>(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
+                              [&](uint32_t v, bool act) {
+                                  return act ? ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v) : 0.0;
+                              },
+                              st);
             if (st.kind == 0) rng.advance();
-            wc.count(st.kind, n - t);
-            const uint32_t slots = (static_cast<uint32_t>(st.pos) & 0xFFu) | (st.mirror << 8);
-            if (due) {
-                ++wc.updates;
-                bump_copy(C, n, cur, st.v, slots, lane);
-            }
-            vis[st.v >> 5] |= 1u << (st.v & 31);
             __syncwarp();
             if (lane == 0) {
-                C.routes[static_cast<size_t>(a) * n + t] = st.v;
                 s.rng = rng;
-                s.len += st.d;
-                s.v = st.v;
-                s.slots = slots;
+                s.kind = st.kind;
+                if (st.kind == 3) {
+                    reqs[atomicAdd(nreq, 1u)] = (static_cast<uint32_t>(wib) << 16) | j;
+                } else {
+                    s.v = st.v;
+                    s.d = st.d;
+                    s.slots = (static_cast<uint32_t>(st.pos) & 0xFFu) | (st.mirror << 8);
+                }
+            }
+            __syncwarp();
+        }
+        // (2) the CTA's full scans, every warp one slice of each
+        __syncthreads();
+        const uint32_t nr = *nreq;
+        if (nr) {  // CTA-uniform
+            for (uint32_t r = 0; r < nr; ++r) {
+                const uint32_t q = reqs[r];
+                const uint32_t ow = q >> 16, oj = q & 0xFFFFu;
+                const uint32_t *vis = vis_cta + (static_cast<size_t>(ow) * A + oj) * I.words;
+                const uint32_t cur = ants_cta[ow * A + oj].cur;
+                const uint32_t wb = wib * slice, we = min(wb + slice, I.words);
+                ScanBest b;
+                if (wb < we)
+                    full_scan_range(I, C, vis, cur,
+                                    [&](uint32_t v, bool act) {
+                                        return act ? ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v) : 0.0;
+                                    },
+                                    lane, wb, we, b);
+                double sc = b.bs;
+                uint32_t node = b.have ? b.bv : 0xffffffffu;
+                warp_argmax_node(sc, node, b.have);
+                const unsigned owner = __ballot_sync(kFull, b.have && b.bv == node);
+                const double tv = __shfl_sync(kFull, b.bt, owner ? __ffs(owner) - 1 : 0);
+                if (lane == 0) parts[r * wpb + wib] = ScanPart{sc, tv, node};
+            }
+            __syncthreads();
+            for (uint32_t r = 0; r < nr; ++r) {
+                const uint32_t q = reqs[r];
+                if ((q >> 16) != static_cast<uint32_t>(wib)) continue;  // warp-uniform
+                DefAnt<RNG> &s = ants[q & 0xFFFFu];
+                // combine the slices: argmax, ties -> lowest id (slices hold disjoint ids)
+                const bool ok = lane < wpb && parts[r * wpb + lane].v != 0xffffffffu;
+                const ScanPart pp = ok ? parts[r * wpb + lane] : ScanPart{0.0, 0.0, 0xffffffffu};
+                double sc = pp.s;
+                uint32_t node = pp.v;
+                warp_argmax_node(sc, node, ok);
+                const unsigned owner = __ballot_sync(kFull, ok && pp.v == node);
+                Step st;
+                finish_scan(I, C, s.cur, node, __shfl_sync(kFull, pp.t, __ffs(owner) - 1), lane, st);
+                __syncwarp();
+                if (lane == 0) {
+                    s.kind = 2;
+                    s.v = st.v;
+                    s.d = st.d;
+                    s.slots = 0xFFu | (st.mirror << 8);
+                }
+                __syncwarp();
+            }
+            __syncthreads();  // every warp has read *nreq and its parts
+            if (threadIdx.x == 0) *nreq = 0;
+        }
+        // (3) bump the counters of this step's edges, record the step
+        for (uint32_t j = 0; j < my_ants; ++j) {
+            const uint32_t a = gw + j * W;
+            uint32_t *vis = vis_base + j * I.words;
+            DefAnt<RNG> &s = ants[j];
+            const uint32_t v = s.v, slots = s.slots;
+            wc.count(s.kind, n - t);
+            if (due) {
+                ++wc.updates;
+                bump_copy(C, n, s.cur, v, slots, lane);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                vis[v >> 5] |= 1u << (v & 31);
+                C.routes[static_cast<size_t>(a) * n + t] = v;
+                s.len += s.d;
             }
             __syncwarp();
         }
@@ -928,7 +1059,6 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
 
     // closing edges: a separate pass after step n-1
     const bool close_due = (n % C.k) == 0;
-    uint32_t close_slots[1] = {0};
     for (uint32_t j = 0; j < my_ants; ++j) {
         const uint32_t a = gw + j * W;
         DefAnt<RNG> &s = ants[j];
@@ -952,7 +1082,6 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
         }
         __syncwarp();
     }
-    (void)close_slots;
     if (close_due) {
         grid_sync(D.bar, gridDim.x);
         for (uint32_t j = 0; j < my_ants; ++j) fold_copy(C, n, ants[j].cur, ants[j].start, ants[j].slots, lane);
@@ -1214,21 +1343,17 @@ static int deferred_launch(const DevInstance &I, const DevColony &C, DevDeferred
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int wpb = kDefBlock / 32;
-    auto smem_for = [&](uint32_t A) {
-        return static_cast<size_t>(wpb) * (32 * sizeof(double) + A * sizeof(DefAnt<RNG>) +
-                                           static_cast<size_t>(A) * I.words * sizeof(uint32_t));
-    };
     uint32_t A = 1;
     size_t smem = 0;
     for (;; ++A) {
-        smem = smem_for(A);
-        if (smem > 200 * 1024) return -1;
+        smem = DefSmem(wpb, A, I.words).bytes;
+        if (smem > 220 * 1024 || A > 0xFFFFu) return -1;
         cudaFuncSetAttribute(k_deferred<RNG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_deferred<RNG>, kDefBlock, smem);
         if (per_sm < 1) return -1;
         if (static_cast<uint64_t>(sms) * per_sm * wpb * A >= C.m) break;
     }
-    const unsigned grid = std::min<unsigned>(sms * per_sm, blocks_for(blocks_for(C.m, A), wpb));
+    const unsigned grid = std::min<unsigned>(sms * per_sm, blocks_for(C.m, A));
     D.ants_per_warp = A;
     void *args[] = {const_cast<DevInstance *>(&I), const_cast<DevColony *>(&C), &D};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void *>(k_deferred<RNG>), grid, kDefBlock, args,

@@ -199,3 +199,23 @@ def test_colony_larger_than_one_wave(acs, orc, gpu, variant):
     assert [int(lens[a]) for a in range(0, m, 97)] == [orc.tour_length(I, routes[a]) for a in range(0, m, 97)]
     assert cnt["local_updates"] == 2 * m * I.n
     assert st["iter_best_len"].tolist()[-1] == lens.min()
+
+
+@pytest.mark.parametrize("mode", ["sync", "seq"])
+def test_no_eta_table_bit_exact(acs, orc, gpu, mode):
+    """n > 4096: no eta^beta table, so every undecided fallback runs the
+    compacted scan (deferred: split over the warps of the CTA).  q0 = 0.5 and
+    few ants keep fallbacks frequent and late, where the pruned pass gives up."""
+    I = small_instance(4200, seed=3, scale=20000)
+    r = pair(acs, orc, I, mode, O.DENSE, m=48 if mode == "sync" else 6, iters=2, seed=2, q0=0.5, k=2)
+    check_exact(*r, O.DENSE)
+    assert r[4]["fallback_full"] > 0
+
+
+def test_sync_cooperative_scan_bit_exact(acs, orc, gpu):
+    """The deferred kernel's full scans split over many warps of a CTA (n = 1002:
+    32 bitmask words, 8 slices) must equal the oracle's single scan."""
+    I = O.load("pr1002")
+    r = pair(acs, orc, I, "sync", O.DENSE, m=64, iters=2, seed=4, q0=0.3)
+    check_exact(*r, O.DENSE)
+    assert r[4]["fallback_full"] > 0
