@@ -15,6 +15,7 @@
 // overlap the next dependent load instead of adding to it.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -315,13 +316,13 @@ __device__ __forceinline__ void rng_init(PhiloxWarp &rng, const DevColony &C, ui
 // Stream commit: roulette commits q (and draws r) here; for a greedy step
 // (o.kind == 0) the caller commits q with rng.advance() AFTER issuing the next
 // row load, which keeps the state transition off the dependent chain.
-template <bool kDefer = false, class RNG, class TauFn>
+template <bool kDefer = false, bool kL32 = false, class RNG, class TauFn>
 __device__ __forceinline__ void select_step(const DevInstance &I, const DevColony &C,
                                             const uint32_t *vis, uint32_t cur, uint4 el,
                                             double tau_lane, RNG &rng, const Lookahead<RNG> &la,
                                             double *scratch, int lane, TauFn tau_of, Step &o) {
     const uint32_t c = el.x & kIdMask;
-    const bool valid = static_cast<uint32_t>(lane) < C.L;
+    const bool valid = kL32 || static_cast<uint32_t>(lane) < C.L;  // kL32: full 32-slot lists
     const bool unv = valid && !visited(vis, c);
     const unsigned um = __ballot_sync(kFull, unv);
     if (um) {
@@ -455,13 +456,28 @@ __device__ __forceinline__ bool copy_index(uint32_t n, uint32_t u, uint32_t v, i
     return lane < 4 && (dense || col < 32u);
 }
 
+// copy_index for k = 1 and lanes 0-2 only (lane 3's copy is written a step
+// late by the row-v lane): no mirror operand
+__device__ __forceinline__ bool copy3_index(uint32_t n, uint32_t u, uint32_t v, int pos, int lane,
+                                            bool &dense, size_t &idx) {
+    // select-only form (no branches): row = u for even lanes, v for lane 1
+    const uint32_t row = (lane & 1) ? v : u;
+    dense = !(lane & 2);
+    const uint32_t col = dense ? (u ^ v ^ row) : static_cast<uint32_t>(pos);
+    idx = static_cast<size_t>(row) * (dense ? n : 32u) + col;
+    return lane < 2 || (lane == 2 && pos >= 0);
+}
+
 // kMode 0 = RELAXED (ACS-GPU-Alt): plain relaxed stores of f(tau_old), lost
 //           updates allowed; also SEQ when launched on one warp.
 // kMode 1 = ATOMIC (CONSISTENT): every local update is one contention-free
 //           `red.add` on a per-copy counter -- no update can be lost and no
 //           ant ever waits on an atomic -- and readers see f^c(base).  The
 //           iteration epilogue folds the counters back into the bases.
-template <int kMode, class RNG, int kRegs = kMaxRegs>
+// kLean: the paper's configuration (k = 1, 32-slot candidate lists) compiled
+// without the update-period counter and the list-length tests, and with the
+// k = 1 copy addressing specialised (lanes 0-2, no mirror operand).
+template <int kMode, class RNG, int kRegs = kMaxRegs, bool kLean = false>
 __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C) {
     constexpr bool kAtomic = kMode == 1;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -510,7 +526,7 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
             Step st;
             if constexpr (kAtomic) {
                 const double tv = trail_value(tl, cl, C, pw_lo, pw_hi);
-                select_step(I, C, vis, cur, el, tv, rng, la, scratch, lane,
+                select_step<false, kLean>(I, C, vis, cur, el, tv, rng, la, scratch, lane,
                             [&](uint32_t v, bool act) {
                                 if (!act) return 0.0;
                                 const size_t k = static_cast<size_t>(cur) * n + v;
@@ -519,7 +535,7 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
                             },
                             st);
             } else {
-                select_step(I, C, vis, cur, el, tl, rng, la, scratch, lane,
+                select_step<false, kLean>(I, C, vis, cur, el, tl, rng, la, scratch, lane,
                             [&](uint32_t v, bool act) {
                                 return act ? ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v) : 0.0;
                             },
@@ -528,7 +544,7 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
             if (st.kind) wc.count(st.kind, n - t);  // greedy steps are derived at flush
             // the copy of the previous edge in THIS row (v -> prev) is written now,
             // by the lane holding prev, after the row's own load has completed
-            if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev) {
+            if ((kLean || static_cast<uint32_t>(lane) < C.L) && (el.x & kIdMask) == mprev) {
                 if constexpr (kAtomic) red_add1(C.cntc + static_cast<size_t>(cur) * 32 + lane);
                 else st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
             }
@@ -542,13 +558,14 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
             el = __ldg(C.rows + ri);
             tl = ld_relaxed(C.tauc + ri);
             if constexpr (kAtomic) cl = ld_relaxed_u32(C.cntc + ri);
-            if (++kc == C.k) {  // D9 per-ant edge counter (warp-uniform)
+            if (kLean || ++kc == C.k) {  // D9 per-ant edge counter (warp-uniform)
                 kc = 0;
-                ++wc.updates;
+                if constexpr (!kLean) ++wc.updates;
                 bool dense;
                 size_t k;
                 // lanes 0-2 now; lane 3's copy (tauc[v][mirror]) one step late, above
-                if (lane < 3 && copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k)) {
+                if (kLean ? copy3_index(n, cur, st.v, st.pos, lane, dense, k)
+                          : (lane < 3 && copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k))) {
                     if constexpr (kAtomic) red_add1((dense ? C.cnt : C.cntc) + k);
                     else st_relaxed((dense ? C.tau : C.tauc) + k, affine(st.tau_old, C.c_l, C.c_0));
                 }
@@ -565,6 +582,7 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
             __syncwarp();
         }
         route_flush(route, rbuf, n - 1, lane);
+        if constexpr (kLean) wc.updates += n - 1;
         // last step's deferred mirror copy (el/tl hold row `cur`)
         if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev) {
             if constexpr (kAtomic) red_add1(C.cntc + static_cast<size_t>(cur) * 32 + lane);
@@ -1269,7 +1287,15 @@ static void launch_tour_kernel(K kernel, const DevInstance &I, const DevColony &
                                cudaStream_t s, bool pw = false) {
     const int threads = one_warp ? 32 : kBlock;
     const int wpb = threads / 32;
-    const unsigned grid = one_warp ? 1u : blocks_for(C.m, wpb);
+    unsigned grid = one_warp ? 1u : blocks_for(C.m, wpb);
+    // Diagnostic: ACS_RESIDENT_ANTS=W caps the ants constructing at once (the
+    // grid-stride loop runs the rest as later waves), to compare the relaxed
+    // variants with the oracle's RELAXED mode at the same concurrency.
+    static const unsigned cap = [] {
+        const char *e = std::getenv("ACS_RESIDENT_ANTS");
+        return e ? static_cast<unsigned>(std::strtoul(e, nullptr, 10)) : 0u;
+    }();
+    if (cap && !one_warp) grid = std::min(grid, std::max(1u, cap / wpb));
     const size_t smem = construct_smem(I, C, wpb, pw);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -1282,9 +1308,9 @@ static void launch_tour_kernel(K kernel, const DevInstance &I, const DevColony &
 // waves instead of four (measured: relaxed 41.9 -> 38.2, atomic 57.9 -> 49.8 ms).
 constexpr int kWideRegs = 72;
 
-template <int kMode, class RNG>
-static void launch_dense(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw = false) {
-    auto narrow = k_construct_dense<kMode, RNG, kMaxRegs>;
+template <int kMode, class RNG, bool kLean>
+static void launch_dense_t(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw) {
+    auto narrow = k_construct_dense<kMode, RNG, kMaxRegs, kLean>;
     if (!one_warp) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
@@ -1294,11 +1320,20 @@ static void launch_dense(const DevInstance &I, const DevColony &C, bool one_warp
             cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, narrow, kBlock, smem);
         if (static_cast<uint64_t>(per_sm) * sms * (kBlock / 32) < C.m) {
-            launch_tour_kernel(k_construct_dense<kMode, RNG, kWideRegs>, I, C, false, s, pw);
+            launch_tour_kernel(k_construct_dense<kMode, RNG, kWideRegs, kLean>, I, C, false, s, pw);
             return;
         }
     }
     launch_tour_kernel(narrow, I, C, one_warp, s, pw);
+}
+
+template <int kMode, class RNG>
+static void launch_dense(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw = false) {
+    if (C.k == 1 && C.L == 32 && !one_warp) {
+        launch_dense_t<kMode, RNG, true>(I, C, one_warp, s, pw);
+        return;
+    }
+    launch_dense_t<kMode, RNG, false>(I, C, one_warp, s, pw);
 }
 
 template <class RNG>

@@ -51,7 +51,7 @@ def main():
     ap.add_argument("--trace-points", type=int, default=200, help="trace samples kept per run (time mode)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    res = {"params": vars(a), "results": {}}
+    res = {"params": dict(vars(a), resident_ants=os.environ.get("ACS_RESIDENT_ANTS")), "results": {}}
     for name in a.instances:
         inst = P.load_instance(name)
         opt = inst.optimum
