@@ -202,6 +202,57 @@ __global__ void __launch_bounds__(1024) k_nn_tour(DevInstance I, uint32_t start,
     if (tid == 0) *out = total + dist_of(I, cur, start, __ldg(I.xs + cur), __ldg(I.ys + cur));
 }
 
+// nn_tour_length with the candidate lists at hand (colony setup): one warp.
+// The lists are sorted by (d, id) (cpp:241-245), so the first unvisited entry
+// of cur's list is the nearest unvisited node with ties -> lowest id, exactly
+// the reference's full-scan pick (cpp:254-280); only when the whole list is
+// visited does the warp scan all n nodes.  ~2% of steps scan, so the setup
+// drops from n block-wide scans to n list probes.
+__global__ void __launch_bounds__(32) k_nn_tour_cand(DevInstance I, const uint32_t *cand, uint32_t L,
+                                                     uint32_t start, int64_t *out) {
+    extern __shared__ uint32_t vis[];
+    const int lane = threadIdx.x & 31;
+    for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
+    __syncwarp();
+    if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
+    __syncwarp();
+    uint32_t cur = start;
+    long long total = 0;
+    for (uint32_t step = 1; step < I.n; ++step) {
+        const double xc = __ldg(I.xs + cur), yc = __ldg(I.ys + cur);
+        const bool in = static_cast<uint32_t>(lane) < L;
+        const uint32_t c = in ? __ldg(cand + static_cast<size_t>(cur) * L + lane) : 0u;
+        const unsigned um = __ballot_sync(kFull, in && !visited(vis, c));
+        uint32_t next;
+        int32_t d;
+        if (um) {
+            next = __shfl_sync(kFull, c, __ffs(um) - 1);
+            d = dist_of(I, cur, next, xc, yc);
+        } else {
+            uint64_t best = ~0ull;
+            for (uint32_t v = lane; v < I.n; v += 32) {
+                if (visited(vis, v)) continue;
+                const int32_t dv = dist_of(I, cur, v, xc, yc);
+                const uint64_t key = (static_cast<uint64_t>(static_cast<uint32_t>(dv)) << 32) | v;
+                best = key < best ? key : best;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t p = shfl_xor_u64(best, o);
+                best = p < best ? p : best;
+            }
+            next = static_cast<uint32_t>(best);
+            d = static_cast<int32_t>(best >> 32);
+        }
+        __syncwarp();
+        if (lane == 0) vis[next >> 5] |= 1u << (next & 31);
+        __syncwarp();
+        total += d;
+        cur = next;
+    }
+    if (lane == 0) *out = total + dist_of(I, cur, start, __ldg(I.xs + cur), __ldg(I.ys + cur));
+}
+
 // K6: warp per route, int64 closed-tour sum (cpp:67-78)
 __global__ void k_tour_lengths(DevInstance I, const uint32_t *routes, uint32_t m, int64_t *out) {
     const int lane = threadIdx.x & 31;
@@ -308,6 +359,11 @@ void launch_build_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, d
 
 void launch_nn_tour(const DevInstance &I, uint32_t start, int64_t *out, cudaStream_t s) {
     k_nn_tour<<<1, 1024, I.words * sizeof(uint32_t), s>>>(I, start, out);
+}
+
+void launch_nn_tour_cand(const DevInstance &I, const uint32_t *cand, uint32_t L, uint32_t start, int64_t *out,
+                         cudaStream_t s) {
+    k_nn_tour_cand<<<1, 32, I.words * sizeof(uint32_t), s>>>(I, cand, L, start, out);
 }
 
 void launch_tour_lengths(const DevInstance &I, const uint32_t *routes, uint32_t m, int64_t *out,
