@@ -320,6 +320,21 @@ def main():
                                      "L2-resident buffer, measured in this run",
                       "ncu_l2_read_bytes_per_launch": sectors * 32 if sectors else None}
 
+    # The construction loop is a dependent chain per ant, so its practical
+    # ceiling is instruction issue (one warp instruction per SM sub-partition
+    # per cycle), not bytes: executed warp instructions per launch (committed
+    # ncu capture) / measured launch time, against 4 x SMs x SM clock.
+    inst = rec.get("instructions")
+    clk_mhz = clk.summary().get("sm_mhz")
+    if inst and clk_mhz:
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        peak_ips = 4 * sms * clk_mhz * 1e6
+        roofline["issue"] = {"achieved": round(inst / construct_s / 1e12, 4), "peak": round(peak_ips / 1e12, 4),
+                             "unit": "T warp-inst/s", "frac": round(inst / construct_s / peak_ips, 4),
+                             "inst_per_launch": inst,
+                             "source": "ncu --set full 'Executed Instructions' of this variant's construct kernel "
+                                       "(profiles/ncu_construct_summary.json) / this run's launch time; peak = "
+                                       "4 schedulers x SMs x median SM clock under load"}
     col.close()
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tours/s", "n_gpus": world,
