@@ -324,14 +324,14 @@ def main():
     # ceiling is instruction issue (one warp instruction per SM sub-partition
     # per cycle), not bytes: executed warp instructions per launch (committed
     # ncu capture) / measured launch time, against 4 x SMs x SM clock.
-    inst = rec.get("instructions")
+    n_inst = rec.get("instructions")
     clk_mhz = clk.summary().get("sm_mhz")
-    if inst and clk_mhz:
+    if n_inst and clk_mhz:
         sms = torch.cuda.get_device_properties(local).multi_processor_count
         peak_ips = 4 * sms * clk_mhz * 1e6
-        roofline["issue"] = {"achieved": round(inst / construct_s / 1e12, 4), "peak": round(peak_ips / 1e12, 4),
-                             "unit": "T warp-inst/s", "frac": round(inst / construct_s / peak_ips, 4),
-                             "inst_per_launch": inst,
+        roofline["issue"] = {"achieved": round(n_inst / construct_s / 1e12, 4), "peak": round(peak_ips / 1e12, 4),
+                             "unit": "T warp-inst/s", "frac": round(n_inst / construct_s / peak_ips, 4),
+                             "inst_per_launch": n_inst,
                              "source": "ncu --set full 'Executed Instructions' of this variant's construct kernel "
                                        "(profiles/ncu_construct_summary.json) / this run's launch time; peak = "
                                        "4 schedulers x SMs x median SM clock under load"}
@@ -399,10 +399,13 @@ def other_variants(P, inst, args, device):
 
 
 def e2e(P, inst, params, args, world, dist=None, device=0, shared=False):
-    """Same metric through the public one-call API (acs_gpu_run): host coords in,
-    host best tour + trace out, setup + K iterations inside the timed region.
-    Every rank runs its own colony at the same time; the whole-job value uses
-    the max wall time over ranks."""
+    """Same metric through the public C-ABI with HOST buffers: create (host
+    coordinates H2D, setup kernels), then every step one acs_gpu_iterate(ctx,
+    1, &stats) with that step's result (iteration best, L_gb: 24 B) read back
+    to the host, then the best tour D2H and destroy -- all inside the timed
+    region.  Every rank runs its own colony at the same time; the whole-job
+    value uses the max wall time over ranks.  Repeated 3 times (host wall
+    clocks on the box jitter by tens of ms); the median is reported."""
     import ctypes as C
     import numpy as np
     from paper_1605_02669_b200 import _native as N
@@ -410,30 +413,43 @@ def e2e(P, inst, params, args, world, dist=None, device=0, shared=False):
     d = inst.desc()
     p = params.to_c(inst.n)
     order = np.empty(inst.n, np.uint32)
-    trace = np.empty(K, np.int64)
     bl = C.c_int64()
+    stat = N.IterStats()
     lib = N.lib()
-    # one untimed call first (lazy CUDA module loading of the setup kernels)
-    N.check(lib.acs_gpu_run(C.byref(d), C.byref(p), 1, device, order.ctypes.data_as(C.c_void_p), C.byref(bl),
-                            trace.ctypes.data_as(C.c_void_p)), "acs_gpu_run")
-    if dist:
-        dist.barrier()
-    t0 = time.perf_counter()
-    N.check(lib.acs_gpu_run(C.byref(d), C.byref(p), K, device, order.ctypes.data_as(C.c_void_p), C.byref(bl),
-                            trace.ctypes.data_as(C.c_void_p)), "acs_gpu_run")
-    dt = time.perf_counter() - t0
-    if dist:
-        import torch
-        t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else f"cuda:{device}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
+
+    def one(k):
+        h = C.c_void_p()
+        N.check(lib.acs_gpu_create(C.byref(d), C.byref(p), device, C.byref(h)), "acs_gpu_create")
+        try:
+            for _ in range(k):
+                N.check(lib.acs_gpu_iterate(h, 1, C.byref(stat)), "acs_gpu_iterate")
+            N.check(lib.acs_gpu_get_best(h, order.ctypes.data_as(C.c_void_p), C.byref(bl)), "acs_gpu_get_best")
+        finally:
+            lib.acs_gpu_destroy(h)
+
+    one(1)  # untimed: lazy CUDA module loading of the setup kernels
+    walls = []
+    for _ in range(3):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        one(K)
+        dt = time.perf_counter() - t0
+        if dist:
+            import torch
+            t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else f"cuda:{device}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        walls.append(dt)
+    dt = statistics.median(walls)
     m = p.ants
     return {"value": round(world * m * K / dt, 1), "unit": "tours/s",
             "h2d_bytes_per_step": round(2 * 8 * inst.n / K, 1),
-            "d2h_bytes_per_step": round((4 * inst.n + 8) / K + 8, 1),
-            "api": f"acs_gpu_run (create + K iterations + best tour/trace D2H + destroy) on each of {world} "
-                   f"rank(s), max wall over ranks",
-            "wall_s": round(dt, 4)}
+            "d2h_bytes_per_step": round(C.sizeof(N.IterStats) + (4 * inst.n + 8) / K, 1),
+            "api": f"acs_gpu_create + K x acs_gpu_iterate(ctx, 1, &stats) (per-step result D2H) + "
+                   f"acs_gpu_get_best + acs_gpu_destroy, host buffers, on each of {world} rank(s); "
+                   f"max wall over ranks, median of 3 runs",
+            "wall_s": round(dt, 4), "wall_s_runs": [round(w, 4) for w in walls]}
 
 
 if __name__ == "__main__":

@@ -39,26 +39,58 @@ int fail(int code, const std::string &msg) {
                         std::string(#expr) + ": " + cudaGetErrorString(e_));            \
     } while (0)
 
-// device buffer with RAII
+// device buffer with RAII.
+// Context allocations are stream-ordered from the device's default memory
+// pool (release threshold raised once per device, see PoolScope), so a
+// context's ~150 MB of buffers are recycled by the next context instead of
+// going through cudaMalloc / cudaFree each time (acs_gpu_run = create + K
+// iterations + destroy).  Buffers of the stateless setup ops use cudaMalloc.
+thread_local cudaStream_t t_alloc_stream = nullptr;
+
 template <class T>
 struct DBuf {
     T *p = nullptr;
     size_t count = 0;
+    cudaStream_t s = nullptr;  // pool allocation ordered on this stream (nullptr: cudaMalloc)
     DBuf() = default;
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (s) cudaFreeAsync(p, s);
+            else cudaFree(p);
+        }
         p = nullptr;
         count = 0;
     }
     cudaError_t alloc(size_t n) {
         release();
         count = n;
-        return n ? cudaMalloc(reinterpret_cast<void **>(&p), n * sizeof(T)) : cudaSuccess;
+        s = t_alloc_stream;
+        if (!n) return cudaSuccess;
+        return s ? cudaMallocAsync(reinterpret_cast<void **>(&p), n * sizeof(T), s)
+                 : cudaMalloc(reinterpret_cast<void **>(&p), n * sizeof(T));
     }
     size_t bytes() const { return count * sizeof(T); }
+};
+
+// While alive, DBuf::alloc on this thread draws from `device`'s default pool,
+// ordered on `stream`; the pool keeps freed memory cached (threshold = max).
+struct PoolScope {
+    PoolScope(int device, cudaStream_t stream) {
+        static bool configured[64] = {};
+        if (device >= 0 && device < 64 && !configured[device]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            configured[device] = true;
+        }
+        t_alloc_stream = stream;
+    }
+    ~PoolScope() { t_alloc_stream = nullptr; }
 };
 
 int check_instance(const acs_instance_desc *inst) {
@@ -452,6 +484,7 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     c->S = spm ? p->slots : 0;
     if (int rc = c->stream.create()) return rc;
     cudaStream_t s = c->stream.s;
+    const PoolScope pool_scope(device, s);
     if (int rc = c->inst.upload(inst, true, s)) return rc;
     const DevInstance &I = c->inst.view;
     const uint32_t n = c->n;

@@ -1,0 +1,31 @@
+"""bench.py contract on the GPU: one short run must print ONE JSON line with
+every key the driver and the judge read (value, e2e, roofline incl. the L2 and
+issue sub-objects, clocks, gpu_launches, cpu_baseline)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def test_bench_json_line(gpu):
+    out = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-variants"],
+                         cwd=REPO, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [x for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "dtype", "data", "config", "roofline", "gpu_launches", "clocks", "e2e", "cpu_baseline"):
+        assert k in d, k
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and 0 < r["frac"] < 1 and r["peak"] > 0
+    assert "l2" in r and 0 < r["l2"]["frac"] < 1
+    assert "issue" in r and 0 < r["issue"]["frac"] < 1
+    assert d["config"]["workload"].startswith("pr2392")
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
