@@ -151,14 +151,22 @@ __device__ __forceinline__ void full_scan_range(const DevInstance &I, const DevC
 }
 
 // The fallback's chosen node `node` (warp-uniform) with its trail value:
-// distance and the mirror slot (where cur sits in node's candidate row).
+// distance and the mirror slot (where cur sits in node's candidate row) --
+// from `mirror` when the caller knows it (next-nearest rows carry it), else
+// by a search of node's row (kMirrorUnknown).
+constexpr uint32_t kMirrorUnknown = 0x100u;
 __device__ __forceinline__ void finish_scan(const DevInstance &I, const DevColony &C, uint32_t cur,
-                                            uint32_t node, double tau_old, int lane, Step &o) {
+                                            uint32_t node, double tau_old, int lane, Step &o,
+                                            uint32_t mirror = kMirrorUnknown) {
     o.v = node;
     o.tau_old = tau_old;
     o.d = tsplib_distance(I.type, __ldg(I.xs + cur), __ldg(I.ys + cur), __ldg(I.xs + node), __ldg(I.ys + node));
     o.pos = -1;
     o.kind = 2;
+    if (mirror != kMirrorUnknown) {
+        o.mirror = mirror;
+        return;
+    }
     const uint32_t id = __ldg(&C.rows[static_cast<size_t>(node) * 32 + lane].x) & kIdMask;
     const unsigned mm = __ballot_sync(kFull, static_cast<uint32_t>(lane) < C.L && id == cur);
     o.mirror = mm ? static_cast<uint32_t>(__ffs(mm) - 1) : kNoMirror;
@@ -188,7 +196,7 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
     uint4 q = C.ext_len ? __ldg(xrow + lane) : make_uint4(kEmpty, 0u, 0u, 0u);
     if (hcnt <= kHot) {
         double bs = 0.0, bt = 0.0;
-        uint32_t bv = 0xffffffffu;
+        uint32_t bv = 0xffffffffu, bm = kMirrorUnknown;  // bm: the best entry's mirror slot
         bool have = false;
         {
             const bool in_list = static_cast<uint32_t>(lane) < hcnt;
@@ -205,11 +213,14 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
         for (uint32_t base = 0; base < C.ext_len; base += 32) {
             if (base) q = __ldg(xrow + base + lane);
             const bool in_list = q.x != kEmpty;
-            const bool act = in_list && !visited(vis, q.x);
-            const double tv = tau_of(in_list ? q.x : 0u, act);
+            const uint32_t qid = q.x & kIdMask;
+            const bool act = in_list && !visited(vis, qid);
+            const double tv = tau_of(in_list ? qid : 0u, act);
             if (act) {
                 const double sc = __dmul_rn(tv, __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z)));
-                if (!have || sc > bs || (sc == bs && q.x < bv)) { have = true; bs = sc; bv = q.x; bt = tv; }
+                if (!have || sc > bs || (sc == bs && qid < bv)) {
+                    have = true; bs = sc; bv = qid; bt = tv; bm = q.x >> 24;
+                }
             }
             double sb = bs;
             uint32_t node = have ? bv : 0xffffffffu;
@@ -220,7 +231,8 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
             const double bound = __dmul_rn(C.tau_bound, __hiloint2double(static_cast<int>(lw), static_cast<int>(lz)));
             if (node != 0xffffffffu && (exhausted || bound < sb)) {
                 const unsigned owner = __ballot_sync(kFull, have && bv == node);
-                finish_scan(I, C, cur, node, __shfl_sync(kFull, bt, __ffs(owner) - 1), lane, o);
+                const int src = __ffs(owner) - 1;
+                finish_scan(I, C, cur, node, __shfl_sync(kFull, bt, src), lane, o, __shfl_sync(kFull, bm, src));
                 return;
             }
         }

@@ -113,10 +113,12 @@ __global__ void k_last_cand_key(DevInstance I, const uint32_t *cand, uint32_t L,
     lower[u] = (static_cast<uint64_t>(static_cast<uint32_t>(d)) << 32) | c;
 }
 
-// slice j of the extended rows {id, d, eta^beta lo, hi} (id = kEmpty past the end);
-// also advances lower[u] to the slice's last key
-__global__ void k_ext_rows(DevInstance I, const uint64_t *keys, uint32_t j, uint32_t ext_len,
-                           double beta, int beta_int, uint4 *ext, uint64_t *lower) {
+// slice j of the extended rows {id | mirror<<24, d, eta^beta lo, hi} (kEmpty
+// past the end; mirror = u's slot in v's candidate list, as in the packed
+// rows, so a fallback settled here needs no extra row load); also advances
+// lower[u] to the slice's last key
+__global__ void k_ext_rows(DevInstance I, const uint32_t *cand, uint32_t L, const uint64_t *keys, uint32_t j,
+                           uint32_t ext_len, double beta, int beta_int, uint4 *ext, uint64_t *lower) {
     const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= static_cast<size_t>(I.n) * 32) return;
     const uint32_t u = static_cast<uint32_t>(idx >> 5), p = static_cast<uint32_t>(idx & 31);
@@ -125,7 +127,11 @@ __global__ void k_ext_rows(DevInstance I, const uint64_t *keys, uint32_t j, uint
     if (key != ~0ull) {
         const int32_t d = static_cast<int32_t>(key >> 32);
         const uint64_t b = dbits(eta_beta(d, beta, beta_int));
-        el = make_uint4(static_cast<uint32_t>(key), static_cast<uint32_t>(d), static_cast<uint32_t>(b),
+        const uint32_t v = static_cast<uint32_t>(key);
+        uint32_t mirror = kNoMirror;
+        for (uint32_t q = 0; q < L; ++q)
+            if (cand[static_cast<size_t>(v) * L + q] == u) { mirror = q; break; }
+        el = make_uint4(v | (mirror << 24), static_cast<uint32_t>(d), static_cast<uint32_t>(b),
                         static_cast<uint32_t>(b >> 32));
     }
     ext[static_cast<size_t>(u) * ext_len + j * 32 + p] = el;
@@ -399,7 +405,7 @@ void launch_ext_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, uin
     for (uint32_t j = 0; j * 32 < ext_len; ++j) {
         k_topk_after<<<blocks_for(I.n, kWarpsPerBlock), kBlock, 0, s>>>(I, scratch_lower, scratch_keys);
         k_ext_rows<<<blocks_for(static_cast<size_t>(I.n) * 32, 256), 256, 0, s>>>(
-            I, scratch_keys, j, ext_len, beta, beta_int, ext, scratch_lower);
+            I, cand, L, scratch_keys, j, ext_len, beta, beta_int, ext, scratch_lower);
     }
 }
 

@@ -1,18 +1,21 @@
 #!/bin/bash
-# Reproduce the paper's m = 256 tables on the GPU (30 seeds, 1000 iterations):
+# Reproduce the paper's m-sweep / k-sweep tables on the GPU.  The paper fixes
+# the BUDGET, not the iteration count: b = 1000 n solutions, so a colony of m
+# ants runs b / m iterations.
 #   PAPER.md:1170-1186  ACS-GPU-Alt (relaxed), m = 256, k in {1,2,4,8,16}, nrw1379 / pr2392
 #   PAPER.md:1211-1240  ACS-GPU-SPM, m = 256, same k sweep (figure; k = 16: 3.72 / 4.66 %)
 #   PAPER.md:1136-1146  ACS-GPU-Alt, k = 1, m in {128, 512, 1024}
 set -u
 mkdir -p gpurun_out
-S=${SEEDS:-30}
-for inst in nrw1379 pr2392; do
-  for k in 1 2 4 8 16; do
+S=${SEEDS:-10}
+for spec in nrw1379:1379 pr2392:2392; do
+  inst=${spec%%:*}; n=${spec##*:}
+  for k in ${KS:-1 2 4 8 16}; do
     python tools/quality.py --instances $inst --variants relaxed spm --ants 256 --k $k --seeds $S \
-      --iterations 1000 --out gpurun_out/qp_${inst}_m256_k$k.json
+      --iterations $((1000 * n / 256)) --out gpurun_out/qb_${inst}_m256_k$k.json
   done
-  for m in 128 512 1024; do
+  for m in ${MS:-128 512 1024}; do
     python tools/quality.py --instances $inst --variants relaxed --ants $m --k 1 --seeds $S \
-      --iterations 1000 --out gpurun_out/qp_${inst}_m${m}_k1.json
+      --iterations $((1000 * n / m)) --out gpurun_out/qb_${inst}_m${m}_k1.json
   done
 done
