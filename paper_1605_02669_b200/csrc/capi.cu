@@ -10,6 +10,7 @@
 #include <cstring>
 #include <algorithm>
 #include <memory>
+#include <mutex>
 
 #ifndef ACS_EXT_MAX
 #define ACS_EXT_MAX 192u // next-nearest entries per row for the pruned fallback (multiple of 32)
@@ -79,14 +80,18 @@ struct DBuf {
 // ordered on `stream`; the pool keeps freed memory cached (threshold = max).
 struct PoolScope {
     PoolScope(int device, cudaStream_t stream) {
+        static std::mutex mu;  // contexts may be created from several host threads (islands)
         static bool configured[64] = {};
-        if (device >= 0 && device < 64 && !configured[device]) {
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-                uint64_t keep = UINT64_MAX;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            if (device >= 0 && device < 64 && !configured[device]) {
+                cudaMemPool_t pool;
+                if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+                    uint64_t keep = UINT64_MAX;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+                }
+                configured[device] = true;
             }
-            configured[device] = true;
         }
         t_alloc_stream = stream;
     }
