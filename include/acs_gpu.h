@@ -87,7 +87,7 @@ typedef struct {
     uint64_t hits, misses;   /* selective memory record updates (local + global) */
     uint64_t fallback_steps; /* steps with every candidate visited */
     uint64_t greedy_steps, roulette_steps;
-    uint64_t cas_retries;    /* atomic variant: failed CAS attempts */
+    uint64_t cas_retries;    /* always 0: the atomic variant's updates are contention-free counters (red.add), no CAS */
     uint64_t iterations;     /* iterations run on this context */
     uint64_t fallback_elems; /* unvisited nodes a full fallback scan covers (algorithmic) */
     uint64_t fallback_full;  /* fallback steps the pruned pass could not settle (full scan run) */

@@ -186,23 +186,6 @@ __device__ __forceinline__ double affine(double tau, double c_mul, double c_add)
     return __dadd_rn(__dmul_rn(c_mul, tau), c_add);
 }
 
-// CONSISTENT read-modify-write of one trail value: CAS loop seeded with the
-// value the caller already holds (no extra load when it is current).
-__device__ __forceinline__ uint32_t cas_affine(double *p, double expect, double c_mul,
-                                               double c_add) {
-    unsigned long long *w = reinterpret_cast<unsigned long long *>(p);
-    unsigned long long e = dbits(expect);
-    uint32_t retries = 0;
-    for (;;) {
-        const unsigned long long nv = dbits(affine(bitsd(e), c_mul, c_add));
-        const unsigned long long got = atomicCAS(w, e, nv);
-        if (got == e) break;
-        e = got;
-        ++retries;
-    }
-    return retries;
-}
-
 // ---------------------------------------------------------------- warp ops
 // argmax over lanes with `valid`, exact on non-negative doubles (their bit
 // patterns order like unsigned integers); ties -> lowest lane (D7).

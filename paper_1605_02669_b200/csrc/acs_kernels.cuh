@@ -91,8 +91,7 @@ struct DevBest {
 // deferred variant: grid-barrier words (arrive count, generation); the per-ant
 // state lives in shared memory of the persistent kernel
 struct DevDeferred {
-    unsigned *bar;             // [320] zero-initialised: gen, 8 group counters, root (128 B apart)
-    uint32_t ants_per_warp;    // set by the launcher
+    uint32_t ants_per_warp;    // set by the launcher (grid barrier: cooperative groups)
 };
 
 // ---- setup launchers (stream-ordered, async) ----

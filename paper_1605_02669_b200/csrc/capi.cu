@@ -220,8 +220,6 @@ struct acs_gpu_ctx {
     DBuf<uint64_t> iter;
     DBuf<unsigned long long> counters;
     DBuf<acs_iter_stats> stats;
-    // deferred variant: grid-barrier words
-    DBuf<unsigned> d_bar;
     // island exchange scratch
     DBuf<int64_t> x_key;
     DBuf<uint32_t> x_tour;
@@ -579,9 +577,7 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     CUDA_TRY(cudaMemcpyAsync(c->best_len.p, &none, sizeof(int64_t), cudaMemcpyHostToDevice, s));
 
     if (p->variant == ACS_VARIANT_DEFERRED) {
-        CUDA_TRY(c->d_bar.alloc(32 * 10));  // generation + 8 group counters + root, 128 B apart
-        CUDA_TRY(cudaMemsetAsync(c->d_bar.p, 0, c->d_bar.bytes(), s));
-        c->deferred = DevDeferred{c->d_bar.p, 1};
+        c->deferred = DevDeferred{1};
     }
 
     DevColony &C = c->colony;

@@ -364,7 +364,7 @@ __device__ __forceinline__ void select_step(const DevInstance &I, const DevColon
 // n < 2^24 steps), flushed and reset once per ant.  greedy is derived at flush
 // time as (steps - roulette - fallback).
 struct WarpCounters {
-    uint32_t fallback = 0, roulette = 0, updates = 0, retry = 0, hits = 0, misses = 0, fb_elems = 0;
+    uint32_t fallback = 0, roulette = 0, updates = 0, hits = 0, misses = 0, fb_elems = 0;
     // unvisited = n - t at step t: the elements a fallback scan touches
     __device__ __forceinline__ void count(int kind, uint32_t unvisited) {
         roulette += kind == 1;
@@ -372,10 +372,8 @@ struct WarpCounters {
         fb_elems += kind == 2 ? unvisited : 0u;
     }
     __device__ __forceinline__ void flush(unsigned long long *c, int lane, uint32_t steps) {
-        const uint32_t retries = __reduce_add_sync(kFull, retry);  // per-lane CAS retries
         if (lane == 0) {
             using ull = unsigned long long;
-            if (retries) atomicAdd(c + kCntCasRetry, static_cast<ull>(retries));
             if (updates) atomicAdd(c + kCntUpdates, static_cast<ull>(updates));
             if (hits) atomicAdd(c + kCntHits, static_cast<ull>(hits));
             if (misses) atomicAdd(c + kCntMisses, static_cast<ull>(misses));
@@ -384,7 +382,7 @@ struct WarpCounters {
             if (roulette) atomicAdd(c + kCntRoulette, static_cast<ull>(roulette));
             if (fb_elems) atomicAdd(c + kCntFallbackElems, static_cast<ull>(fb_elems));
         }
-        fallback = roulette = updates = retry = hits = misses = fb_elems = 0;
+        fallback = roulette = updates = hits = misses = fb_elems = 0;
     }
 };
 
@@ -849,7 +847,7 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
 // cooperative_groups' grid sync measured 1.3 us per barrier on B200 at
 // 148 x 640 threads, against 2.6 us for a two-level atomic-counter barrier
 // and 1.9 us for a flat acquire/release one (tools/micro/grid_barrier.cu).
-__device__ __forceinline__ void grid_sync(unsigned *, unsigned) { cg::this_grid().sync(); }
+__device__ __forceinline__ void grid_sync() { cg::this_grid().sync(); }
 
 template <class RNG>
 struct DefAnt {             // per-ant state of the deferred variant, in shared memory
@@ -971,7 +969,7 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
         }
         __syncwarp();
     }
-    grid_sync(D.bar, gridDim.x);
+    grid_sync();
 
     for (uint32_t t = 1; t < n; ++t) {
         const bool due = (t % C.k) == 0;
@@ -1076,7 +1074,7 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
             }
             __syncwarp();
         }
-        grid_sync(D.bar, gridDim.x);
+        grid_sync();
         for (uint32_t j = 0; j < my_ants; ++j) {
             DefAnt<RNG> &s = ants[j];
             if (due) fold_copy(C, n, s.cur, s.v, s.slots, lane);
@@ -1084,7 +1082,7 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
             if (lane == 0) s.cur = s.v;
             __syncwarp();
         }
-        if (due) grid_sync(D.bar, gridDim.x);
+        if (due) grid_sync();
     }
 
     // closing edges: a separate pass after step n-1
@@ -1113,7 +1111,7 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
         __syncwarp();
     }
     if (close_due) {
-        grid_sync(D.bar, gridDim.x);
+        grid_sync();
         for (uint32_t j = 0; j < my_ants; ++j) fold_copy(C, n, ants[j].cur, ants[j].start, ants[j].slots, lane);
     }
     wc.flush(C.counters, lane, my_ants * (n - 1));
