@@ -8,14 +8,16 @@
 set -u
 mkdir -p gpurun_out
 S=${SEEDS:-10}
-for spec in nrw1379:1379 pr2392:2392; do
+S0=${SEED0:-0}
+TAG=${TAG:-qb}
+for spec in ${SPECS:-nrw1379:1379 pr2392:2392}; do
   inst=${spec%%:*}; n=${spec##*:}
   for k in ${KS:-1 2 4 8 16}; do
-    python tools/quality.py --instances $inst --variants relaxed spm --ants 256 --k $k --seeds $S \
-      --iterations $((1000 * n / 256)) --out gpurun_out/qb_${inst}_m256_k$k.json
+    python tools/quality.py --instances $inst --variants relaxed spm --ants 256 --k $k --seeds $S --seed0 $S0 \
+      --iterations $((1000 * n / 256)) --out gpurun_out/${TAG}_${inst}_m256_k$k.json
   done
   for m in ${MS:-128 512 1024}; do
-    python tools/quality.py --instances $inst --variants relaxed --ants $m --k 1 --seeds $S \
-      --iterations $((1000 * n / m)) --out gpurun_out/qb_${inst}_m${m}_k1.json
+    python tools/quality.py --instances $inst --variants relaxed --ants $m --k 1 --seeds $S --seed0 $S0 \
+      --iterations $((1000 * n / m)) --out gpurun_out/${TAG}_${inst}_m${m}_k1.json
   done
 done
