@@ -335,6 +335,24 @@ def main():
                              "source": "ncu --set full 'Executed Instructions' of this variant's construct kernel "
                                        "(profiles/ncu_construct_summary.json) / this run's launch time; peak = "
                                        "4 schedulers x SMs x median SM clock under load"}
+    # Latency bound: every ant is a chain of n-1 dependent steps, so no colony
+    # can construct faster than ONE isolated ant's tour.  A 128-ant colony
+    # (< 1 ant per SM, no issue contention) of the same variant measures that
+    # chain in this run; frac = its construct time / the full colony's.
+    p_lat = P.AcsParams(variant=args.variant, m=128, k=args.k, seed=args.seed, rng=rng_for(args.variant, args.rng))
+    with P.Colony(inst, p_lat, device=local) as lc:
+        lc.iterate(2)
+        lat = []
+        for i in range(5):
+            flush.fill_(i & 0xFF)
+            torch.cuda.synchronize()
+            lc.iterate(1)
+            lat.append(lc.last_timing()[1])
+    lat_ms = statistics.median(lat)
+    roofline["latency"] = {"bound_ms": round(lat_ms, 4), "achieved_ms": round(construct_s * 1e3, 4),
+                           "frac": round(lat_ms / (construct_s * 1e3), 4),
+                           "source": "construct time of a 128-ant colony (same variant, < 1 ant per SM: the "
+                                     "isolated dependent chain of n-1 steps), median of 5, measured in this run"}
     col.close()
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tours/s", "n_gpus": world,

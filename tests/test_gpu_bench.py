@@ -27,5 +27,6 @@ def test_bench_json_line(gpu):
     assert r["bound"] == "hbm" and 0 < r["frac"] < 1 and r["peak"] > 0
     assert "l2" in r and 0 < r["l2"]["frac"] < 1
     assert "issue" in r and 0 < r["issue"]["frac"] < 1
+    assert "latency" in r and 0 < r["latency"]["frac"] <= 1.2
     assert d["config"]["workload"].startswith("pr2392")
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
