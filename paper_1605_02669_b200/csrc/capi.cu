@@ -317,7 +317,13 @@ int acs_gpu_nn_tour_length(const acs_instance_desc *inst, uint32_t start, int de
     if (int rc = di.upload(inst, true, st.s)) return rc;
     DBuf<int64_t> d;
     CUDA_TRY(d.alloc(1));
-    launch_nn_tour(di.view, start, d.p, st.s);
+    // candidate lists first (K2, tens of us): the NN walk then probes the
+    // first unvisited list entry and scans all n only when a list is exhausted
+    const uint32_t L = inst->n - 1 < 32u ? inst->n - 1 : 32u;
+    DBuf<uint32_t> cand;
+    CUDA_TRY(cand.alloc(static_cast<size_t>(inst->n) * L));
+    launch_topk(di.view, L, cand.p, st.s);
+    launch_nn_tour_cand(di.view, cand.p, L, start, d.p, st.s);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(out, d.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st.s));
     CUDA_TRY(cudaStreamSynchronize(st.s));

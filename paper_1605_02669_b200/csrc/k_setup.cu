@@ -3,7 +3,7 @@
 //   K2 k_topk             tsp_instance.cpp:219-252 build_candidates (bit-exact)
 //      k_build_rows       packed candidate rows: id | mirror, distance, eta^beta
 //      k_eta_table        eta^beta of every edge (fallback scan operand, n <= 4096)
-//      k_nn_tour          tsp_instance.cpp:254-280 nn_tour_length -> tau0
+//      k_nn_tour_cand     tsp_instance.cpp:254-280 nn_tour_length -> tau0 (candidate-list probe + full scan)
 //   K6 k_tour_lengths     tsp_instance.cpp:67-78 tour_length (validation / eval)
 //   plus device RNG and selective-store op scripts used by the parity tests.
 #include <algorithm>
@@ -157,55 +157,6 @@ __global__ void k_build_rows(DevInstance I, const uint32_t *cand, uint32_t L, do
                         static_cast<uint32_t>(b >> 32));
     }
     rows[idx] = el;
-}
-
-// nn_tour_length: one CTA, per step a block argmin of (d<<32 | v) over the
-// unvisited nodes (strict < in ascending v == min key), cpp:254-280.
-__global__ void __launch_bounds__(1024) k_nn_tour(DevInstance I, uint32_t start, int64_t *out) {
-    extern __shared__ uint32_t vis[];
-    __shared__ uint64_t red[32];
-    __shared__ uint64_t pick;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (uint32_t i = tid; i < I.words; i += blockDim.x) vis[i] = 0;
-    __syncthreads();
-    if (tid == 0) vis[start >> 5] |= 1u << (start & 31);
-    __syncthreads();
-    uint32_t cur = start;
-    int64_t total = 0;
-    for (uint32_t step = 1; step < I.n; ++step) {
-        const double xc = __ldg(I.xs + cur), yc = __ldg(I.ys + cur);
-        uint64_t best = ~0ull;
-        for (uint32_t v = tid; v < I.n; v += blockDim.x) {
-            if (visited(vis, v)) continue;
-            const int32_t d = dist_of(I, cur, v, xc, yc);
-            const uint64_t key = (static_cast<uint64_t>(static_cast<uint32_t>(d)) << 32) | v;
-            best = key < best ? key : best;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const uint64_t p = shfl_xor_u64(best, o);
-            best = p < best ? p : best;
-        }
-        if (lane == 0) red[wid] = best;
-        __syncthreads();
-        if (wid == 0) {
-            uint64_t b = lane < static_cast<int>(blockDim.x >> 5) ? red[lane] : ~0ull;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const uint64_t p = shfl_xor_u64(b, o);
-                b = p < b ? p : b;
-            }
-            if (lane == 0) {
-                pick = b;
-                const uint32_t v = static_cast<uint32_t>(b);
-                vis[v >> 5] |= 1u << (v & 31);
-            }
-        }
-        __syncthreads();
-        total += static_cast<int64_t>(pick >> 32);
-        cur = static_cast<uint32_t>(pick);
-    }
-    if (tid == 0) *out = total + dist_of(I, cur, start, __ldg(I.xs + cur), __ldg(I.ys + cur));
 }
 
 // nn_tour_length with the candidate lists at hand (colony setup): one warp.
@@ -363,9 +314,6 @@ void launch_build_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, d
                                                                                 beta_int, rows);
 }
 
-void launch_nn_tour(const DevInstance &I, uint32_t start, int64_t *out, cudaStream_t s) {
-    k_nn_tour<<<1, 1024, I.words * sizeof(uint32_t), s>>>(I, start, out);
-}
 
 void launch_nn_tour_cand(const DevInstance &I, const uint32_t *cand, uint32_t L, uint32_t start, int64_t *out,
                          cudaStream_t s) {
