@@ -8,6 +8,7 @@
 //   DENSE     x RELAXED -> ACS_VARIANT_ATOMIC    (CONSISTENT, CAS)  or
 //                          ACS_VARIANT_RELAXED   (consistent=false: ACS-GPU-Alt lost updates)
 //   SELECTIVE x SEQ     -> ACS_VARIANT_SPM_SEQ
+//   SELECTIVE x SYNC    -> ACS_VARIANT_SPM_SYNC  (step snapshot + ordered record updates; deterministic)
 //   SELECTIVE x RELAXED -> ACS_VARIANT_SPM       (ACS-GPU-SPM)
 #pragma once
 
@@ -23,7 +24,7 @@ namespace acs {
 
 enum class Mode { kSeq, kSync, kRelaxed };
 enum class Memory { kDense, kSelective };
-enum class Variant { kAuto, kAtomic, kDeferred, kRelaxed, kSpm, kSeq, kSpmSeq };
+enum class Variant { kAuto, kAtomic, kDeferred, kRelaxed, kSpm, kSeq, kSpmSeq, kSpmSync };
 enum class RngKind { kXoshiro, kPhilox };
 
 struct AcsParams {

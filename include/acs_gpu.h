@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define ACS_GPU_ABI_VERSION 2  /* 2: acs_counters.fallback_full, acs_random_instance */
+#define ACS_GPU_ABI_VERSION 3  /* 2: acs_counters.fallback_full, acs_random_instance; 3: ACS_VARIANT_SPM_SYNC */
 
 /* status codes */
 #define ACS_OK 0
@@ -47,7 +47,8 @@ enum acs_variant {
     ACS_VARIANT_RELAXED = 2,  /* dense matrix, plain relaxed ld/st, lost updates allowed (ACS-GPU-Alt) */
     ACS_VARIANT_SPM = 3,      /* selective pheromone memory, relaxed (ACS-GPU-SPM) */
     ACS_VARIANT_SEQ = 4,      /* dense, SPEC SEQ (ant-major, immediate updates) on one warp */
-    ACS_VARIANT_SPM_SEQ = 5   /* selective memory, SPEC SEQ on one warp */
+    ACS_VARIANT_SPM_SEQ = 5,  /* selective memory, SPEC SEQ on one warp */
+    ACS_VARIANT_SPM_SYNC = 6  /* selective memory, SPEC SYNC: step snapshot, ordered apply (parity mode, m <= 8192) */
 };
 
 enum acs_rng_kind { ACS_RNG_XOSHIRO = 0, ACS_RNG_PHILOX = 1 };

@@ -18,11 +18,11 @@ LIB_PATH = os.path.join(HERE, f"libacs_b200_{_suffix}.so" if _suffix else "libac
 
 ACS_OK, ACS_E_ARG, ACS_E_CUDA, ACS_E_NOMEM, ACS_E_NCCL, ACS_E_PARSE = 0, -1, -2, -3, -4, -5
 EUC_2D, CEIL_2D, ATT = 0, 1, 2
-VARIANT_ATOMIC, VARIANT_DEFERRED, VARIANT_RELAXED, VARIANT_SPM, VARIANT_SEQ, VARIANT_SPM_SEQ = range(6)
+VARIANT_ATOMIC, VARIANT_DEFERRED, VARIANT_RELAXED, VARIANT_SPM, VARIANT_SEQ, VARIANT_SPM_SEQ, VARIANT_SPM_SYNC = range(7)
 RNG_XOSHIRO, RNG_PHILOX = 0, 1
 
 VARIANTS = {"atomic": VARIANT_ATOMIC, "deferred": VARIANT_DEFERRED, "relaxed": VARIANT_RELAXED,
-            "spm": VARIANT_SPM, "seq": VARIANT_SEQ, "spm-seq": VARIANT_SPM_SEQ}
+            "spm": VARIANT_SPM, "seq": VARIANT_SEQ, "spm-seq": VARIANT_SPM_SEQ, "spm-sync": VARIANT_SPM_SYNC}
 
 
 class InstanceDesc(C.Structure):

@@ -90,6 +90,13 @@ struct DevBest {
 
 // deferred variant: grid-barrier words (arrive count, generation); the per-ant
 // state lives in shared memory of the persistent kernel
+// SYNC x SELECTIVE (parity mode): per-ant state, visited bitmasks, step ops
+struct DevSpmSync {
+    void *ants;            // m x SyncAnt<RNG>
+    uint32_t *vis;         // m x words
+    uint4 *ops;            // 2m {key lo, key hi, neighbour, 0}
+};
+
 struct DevDeferred {
     uint32_t ants_per_warp;    // set by the launcher (grid barrier: cooperative groups)
 };
@@ -130,6 +137,8 @@ int launch_deferred(int rng, const DevInstance &I, const DevColony &C, const Dev
                     cudaStream_t s);
 // eval-free epilogue: iteration best (ties lowest ant), strict global best,
 // global update on the best tour, stats[slot], iter++
+int launch_spm_sync(int rng, const DevInstance &I, const DevColony &C, const DevSpmSync &Y, cudaStream_t s);
+size_t spm_sync_ant_bytes();
 void launch_epilogue(bool spm, bool fold, const DevInstance &I, const DevColony &C,
                      const DevBest &B, uint32_t slot, cudaStream_t s);
 // island import: adopt (tour,len) from device buffers if strictly better

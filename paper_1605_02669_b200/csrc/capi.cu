@@ -232,12 +232,19 @@ struct acs_gpu_ctx {
     DevColony colony{};
     DevBest best{};
     DevDeferred deferred{};
+    DBuf<unsigned char> sy_ants;  // SYNC x SELECTIVE: per-ant state, bitmasks, step ops
+    DBuf<uint32_t> sy_vis;
+    DBuf<uint4> sy_ops;
+    DevSpmSync spm_sync{};
 
     ~acs_gpu_ctx() {
         if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
         for (cudaEvent_t e : events) cudaEventDestroy(e);
     }
-    bool dense() const { return params.variant != ACS_VARIANT_SPM && params.variant != ACS_VARIANT_SPM_SEQ; }
+    bool dense() const {
+        return params.variant != ACS_VARIANT_SPM && params.variant != ACS_VARIANT_SPM_SEQ &&
+               params.variant != ACS_VARIANT_SPM_SYNC;
+    }
     int ensure_events(size_t count) {
         while (events.size() < count) {
             cudaEvent_t e;
@@ -472,13 +479,14 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     if (!p) return fail(ACS_E_ARG, "null params");
     if (p->cl < 1 || p->cl > 32) return fail(ACS_E_ARG, "cl must be in [1, 32] on the GPU path");
     if (p->update_period < 1) return fail(ACS_E_ARG, "update_period (k) must be >= 1");
-    if (p->variant > ACS_VARIANT_SPM_SEQ) return fail(ACS_E_ARG, "unknown variant");
+    if (p->variant > ACS_VARIANT_SPM_SYNC) return fail(ACS_E_ARG, "unknown variant");
     if (p->rng > ACS_RNG_PHILOX) return fail(ACS_E_ARG, "unknown rng");
     if (!(p->rho > 0.0 && p->rho < 1.0)) return fail(ACS_E_ARG, "rho (local evaporation) must be in (0,1)");
     if (!(p->alpha > 0.0 && p->alpha < 1.0)) return fail(ACS_E_ARG, "alpha (global evaporation) must be in (0,1)");
     if (p->q0 > 1.0) return fail(ACS_E_ARG, "q0 must be <= 1");
     if (!(p->beta >= 0.0)) return fail(ACS_E_ARG, "beta must be >= 0");
-    const bool spm = p->variant == ACS_VARIANT_SPM || p->variant == ACS_VARIANT_SPM_SEQ;
+    const bool spm = p->variant == ACS_VARIANT_SPM || p->variant == ACS_VARIANT_SPM_SEQ ||
+                     p->variant == ACS_VARIANT_SPM_SYNC;
     if (spm && !(p->slots == 1 || p->slots == 2 || p->slots == 4 || p->slots == 8 || p->slots == 16))
         return fail(ACS_E_ARG, "slots must be one of 1,2,4,8,16");
     if (int rc = set_device(device)) return rc;
@@ -585,6 +593,14 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     if (p->variant == ACS_VARIANT_DEFERRED) {
         c->deferred = DevDeferred{1};
     }
+    if (p->variant == ACS_VARIANT_SPM_SYNC) {
+        // the apply pass sorts the step's 2m ops in one CTA's shared memory
+        if (c->m > 8192) return fail(ACS_E_ARG, "spm-sync (SYNC x SELECTIVE parity mode) supports m <= 8192");
+        CUDA_TRY(c->sy_ants.alloc(static_cast<size_t>(c->m) * spm_sync_ant_bytes()));
+        CUDA_TRY(c->sy_vis.alloc(static_cast<size_t>(c->m) * I.words));
+        CUDA_TRY(c->sy_ops.alloc(static_cast<size_t>(c->m) * 2));
+        c->spm_sync = DevSpmSync{c->sy_ants.p, c->sy_vis.p, c->sy_ops.p};
+    }
 
     DevColony &C = c->colony;
     C.m = c->m;
@@ -667,6 +683,9 @@ int acs_gpu_iterate(acs_gpu_ctx *c, uint32_t n_iter, acs_iter_stats *out) {
             if (launch_deferred(rng, I, c->colony, c->deferred, s) != 0)
                 return fail(ACS_E_CUDA, std::string("deferred: cooperative launch failed (colony not co-resident): ") +
                                             cudaGetErrorString(cudaGetLastError()));
+        } else if (variant == ACS_VARIANT_SPM_SYNC) {
+            if (launch_spm_sync(rng, I, c->colony, c->spm_sync, s) != 0)
+                return fail(ACS_E_CUDA, std::string("spm-sync launch failed: ") + cudaGetErrorString(cudaGetLastError()));
         } else {
             launch_construct(variant, rng, I, c->colony, s);
         }

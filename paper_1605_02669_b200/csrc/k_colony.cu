@@ -1117,6 +1117,205 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
     wc.flush(C.counters, lane, my_ants * (n - 1));
 }
 
+// ============================================================ SYNC x SELECTIVE
+
+// SPEC SYNC over the selective memory (the oracle's SYNC mode with SELECTIVE
+// memory): every step all ants select against the step-start records, then
+// the step's local updates are applied in ant order -- per ant record u then
+// record v (D4).  Inserts into a record do not commute (FIFO eviction), so the
+// apply pass sorts the step's 2m record operations by (record, ant, u/v) and
+// one thread walks each record's operations in that order.  Deterministic,
+// bit-exact with the oracle; a parity mode, launched per step.
+
+template <class RNG>
+struct SyncAnt {              // per-ant state between the per-step launches
+    RNG rng;
+    long long len;
+    uint32_t cur, start;
+    uint32_t roulette, fallback, fb_elems;
+};
+
+// op key: record << 32 | ant << 1 | (0: record u gets v, 1: record v gets u);
+// payload: the neighbour
+__device__ __forceinline__ void post_op(uint4 *ops, uint32_t i, uint32_t record, uint32_t ant, uint32_t sub,
+                                        uint32_t nb) {
+    const uint64_t key = (static_cast<uint64_t>(record) << 32) | (ant << 1) | sub;
+    ops[i] = make_uint4(static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32), nb, 0u);
+}
+
+template <class RNG>
+__global__ void k_ssync_init(DevInstance I, DevColony C, DevSpmSync Y) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (a >= C.m) return;
+    uint32_t *vis = Y.vis + static_cast<size_t>(a) * I.words;
+    for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
+    RNG rng;
+    rng_init(rng, C, *C.iter, a);
+    const uint32_t start = static_cast<uint32_t>(uniform_int(rng, I.n));
+    __syncwarp();
+    if (lane == 0) {
+        vis[start >> 5] |= 1u << (start & 31);
+        SyncAnt<RNG> &s = reinterpret_cast<SyncAnt<RNG> *>(Y.ants)[a];
+        s.rng = rng;
+        s.len = 0;
+        s.cur = s.start = start;
+        s.roulette = s.fallback = s.fb_elems = 0;
+        C.routes[static_cast<size_t>(a) * I.n] = start;
+    }
+}
+
+template <class RNG>
+__global__ void __maxnreg__(kMaxRegs) k_ssync_select(DevInstance I, DevColony C, DevSpmSync Y, uint32_t t,
+                                                     int due) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
+    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + wib;
+    if (a >= C.m) return;
+    SyncAnt<RNG> &s = reinterpret_cast<SyncAnt<RNG> *>(Y.ants)[a];
+    const uint32_t *vis = Y.vis + static_cast<size_t>(a) * I.words;
+    const uint32_t cur = s.cur;
+    RNG rng = s.rng;
+    const uint4 el = __ldg(C.rows + static_cast<size_t>(cur) * 32 + lane);
+    // the step-start record of cur: slot j in lane j
+    const bool mine = static_cast<uint32_t>(lane) < C.S;
+    const double val = mine ? ld_relaxed(C.spm.vals(cur) + lane) : 0.0;
+    const uint32_t idl = mine ? ld_relaxed_u32(C.spm.ids(cur) + lane) : kEmpty;
+    auto lookup = [&](uint32_t v) {  // all lanes call; first matching slot
+        int hit = -1;
+        for (int j = static_cast<int>(C.S) - 1; j >= 0; --j)
+            if (__shfl_sync(kFull, idl, j) == v) hit = j;
+        const double x = __shfl_sync(kFull, val, hit < 0 ? 0 : hit);
+        return hit < 0 ? C.tau_min : x;
+    };
+    const double tau_lane = lookup(el.x & kIdMask);
+    Lookahead<RNG> la;
+    la.prepare(rng);
+    Step st;
+    select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
+                [&](uint32_t v, bool act) { return lookup(act ? v : kEmpty); }, st);
+    if (st.kind == 0) rng.advance();
+    __syncwarp();
+    if (lane == 0) {
+        Y.vis[static_cast<size_t>(a) * I.words + (st.v >> 5)] |= 1u << (st.v & 31);
+        C.routes[static_cast<size_t>(a) * I.n + t] = st.v;
+        s.rng = rng;
+        s.len += st.d;
+        s.cur = st.v;
+        s.roulette += st.kind == 1;
+        s.fallback += st.kind == 2;
+        s.fb_elems += st.kind == 2 ? I.n - t : 0u;
+        if (due) {
+            post_op(Y.ops, 2 * a, cur, a, 0, st.v);
+            post_op(Y.ops, 2 * a + 1, st.v, a, 1, cur);
+        } else {
+            Y.ops[2 * a] = Y.ops[2 * a + 1] = make_uint4(kEmpty, kEmpty, 0u, 0u);
+        }
+    }
+}
+
+// closing edges (after step n-1): lengths, counters, and the closing ops
+template <class RNG>
+__global__ void k_ssync_close(DevInstance I, DevColony C, DevSpmSync Y, int due) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (a >= C.m) return;
+    SyncAnt<RNG> &s = reinterpret_cast<SyncAnt<RNG> *>(Y.ants)[a];
+    (void)lane;
+    const int32_t d = tsplib_distance(I.type, __ldg(I.xs + s.cur), __ldg(I.ys + s.cur), __ldg(I.xs + s.start),
+                                      __ldg(I.ys + s.start));
+    if (lane == 0) {
+        C.lens[a] = s.len + d;
+        if (due) {
+            post_op(Y.ops, 2 * a, s.cur, a, 0, s.start);
+            post_op(Y.ops, 2 * a + 1, s.start, a, 1, s.cur);
+        } else {
+            Y.ops[2 * a] = Y.ops[2 * a + 1] = make_uint4(kEmpty, kEmpty, 0u, 0u);
+        }
+        using ull = unsigned long long;
+        const uint32_t steps = I.n - 1;
+        const uint32_t updates = (steps / C.k) + (due ? 1u : 0u);
+        atomicAdd(C.counters + kCntUpdates, static_cast<ull>(updates));
+        atomicAdd(C.counters + kCntGreedy, static_cast<ull>(steps - s.roulette - s.fallback));
+        if (s.roulette) atomicAdd(C.counters + kCntRoulette, static_cast<ull>(s.roulette));
+        if (s.fallback) atomicAdd(C.counters + kCntFallback, static_cast<ull>(s.fallback));
+        if (s.fb_elems) atomicAdd(C.counters + kCntFallbackElems, static_cast<ull>(s.fb_elems));
+    }
+}
+
+// One CTA: bitonic sort of the step's 2m op keys (with their index), then
+// every record's operations applied in (ant, u/v) order by one thread.
+__global__ void __launch_bounds__(1024) k_ssync_apply(DevColony C, DevSpmSync Y, uint32_t count, uint32_t pow2) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t *key = reinterpret_cast<uint64_t *>(smem);
+    uint32_t *idx = reinterpret_cast<uint32_t *>(key + pow2);
+    for (uint32_t i = threadIdx.x; i < pow2; i += blockDim.x) {
+        if (i < count) {
+            const uint4 o = Y.ops[i];
+            key[i] = (static_cast<uint64_t>(o.y) << 32) | o.x;
+        } else {
+            key[i] = ~0ull;
+        }
+        idx[i] = i;
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= pow2; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < pow2; i += blockDim.x) {
+                const uint32_t l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    if ((key[i] > key[l]) == up) {
+                        const uint64_t tk = key[i]; key[i] = key[l]; key[l] = tk;
+                        const uint32_t ti = idx[i]; idx[i] = idx[l]; idx[l] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    unsigned long long hits = 0, misses = 0;
+    for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+        if (key[i] == ~0ull) continue;
+        const uint32_t r = static_cast<uint32_t>(key[i] >> 32);
+        if (i > 0 && static_cast<uint32_t>(key[i - 1] >> 32) == r) continue;  // not a segment head
+        for (uint32_t j = i; j < count && key[j] != ~0ull && static_cast<uint32_t>(key[j] >> 32) == r; ++j) {
+            const uint4 o = Y.ops[idx[j]];
+            if (spm_update_mem(C.spm, r, o.z, C.c_l, C.c_0, C.tau_min, nullptr)) ++hits; else ++misses;
+        }
+    }
+    if (hits) atomicAdd(C.counters + kCntHits, hits);
+    if (misses) atomicAdd(C.counters + kCntMisses, misses);
+}
+
+template <class RNG>
+static int spm_sync_iteration(const DevInstance &I, const DevColony &C, const DevSpmSync &Y, cudaStream_t s) {
+    const unsigned wpb = 4, grid = blocks_for(C.m, wpb);
+    const uint32_t count = 2 * C.m;
+    uint32_t pow2 = 1;
+    while (pow2 < count) pow2 <<= 1;
+    const size_t apply_smem = static_cast<size_t>(pow2) * (sizeof(uint64_t) + sizeof(uint32_t));
+    if (apply_smem > 200 * 1024) return -1;
+    cudaFuncSetAttribute(k_ssync_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(apply_smem));
+    k_ssync_init<RNG><<<grid, wpb * 32, 0, s>>>(I, C, Y);
+    for (uint32_t t = 1; t < I.n; ++t) {
+        const int due = (t % C.k) == 0;
+        k_ssync_select<RNG><<<grid, wpb * 32, wpb * 32 * sizeof(double), s>>>(I, C, Y, t, due);
+        if (due) k_ssync_apply<<<1, 1024, apply_smem, s>>>(C, Y, count, pow2);
+    }
+    const int close_due = (I.n % C.k) == 0;
+    k_ssync_close<RNG><<<grid, wpb * 32, 0, s>>>(I, C, Y, close_due);
+    if (close_due) k_ssync_apply<<<1, 1024, apply_smem, s>>>(C, Y, count, pow2);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_spm_sync(int rng, const DevInstance &I, const DevColony &C, const DevSpmSync &Y, cudaStream_t s) {
+    return rng == ACS_RNG_PHILOX ? spm_sync_iteration<Philox>(I, C, Y, s) : spm_sync_iteration<Xoshiro>(I, C, Y, s);
+}
+
+size_t spm_sync_ant_bytes() { return std::max(sizeof(SyncAnt<Philox>), sizeof(SyncAnt<Xoshiro>)); }
+
 // ============================================================ iteration end
 
 // select_best (ties -> lowest ant), strict is_better, best

@@ -34,6 +34,7 @@ const char *variant_name(int v) {
         case ACS_VARIANT_SPM: return "spm";
         case ACS_VARIANT_SEQ: return "seq";
         case ACS_VARIANT_SPM_SEQ: return "spm-seq";
+        case ACS_VARIANT_SPM_SYNC: return "spm-sync";
     }
     return "?";
 }
@@ -76,6 +77,7 @@ int resolve_variant(const AcsParams &p) {
         case Variant::kSpm: return ACS_VARIANT_SPM;
         case Variant::kSeq: return ACS_VARIANT_SEQ;
         case Variant::kSpmSeq: return ACS_VARIANT_SPM_SEQ;
+        case Variant::kSpmSync: return ACS_VARIANT_SPM_SYNC;
         case Variant::kAuto: break;
     }
     if (p.memory == Memory::kDense) {
@@ -84,8 +86,7 @@ int resolve_variant(const AcsParams &p) {
         return p.consistent ? ACS_VARIANT_ATOMIC : ACS_VARIANT_RELAXED;
     }
     if (p.mode == Mode::kSeq) return ACS_VARIANT_SPM_SEQ;
-    if (p.mode == Mode::kSync)
-        throw std::invalid_argument("SYNC mode with SELECTIVE memory is not provided on the GPU path");
+    if (p.mode == Mode::kSync) return ACS_VARIANT_SPM_SYNC;
     return ACS_VARIANT_SPM;
 }
 

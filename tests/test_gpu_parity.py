@@ -4,6 +4,7 @@ oracle (SPEC restatement).  Deterministic variants must be BIT-EXACT:
   GPU ACS_VARIANT_SEQ      (k_construct_dense, one warp)  == oracle SEQ   / DENSE
   GPU ACS_VARIANT_DEFERRED (k_def_select/apply, all ants) == oracle SYNC  / DENSE
   GPU ACS_VARIANT_SPM_SEQ  (k_construct_spm, one warp)    == oracle SEQ   / SELECTIVE
+  GPU ACS_VARIANT_SPM_SYNC (k_ssync_*, all ants, sorted ordered apply) == oracle SYNC / SELECTIVE
 
 compared on: per-iteration L_gb trace, iteration-best length and ant, every
 route and length of the last iteration, the final pheromone state (dense
@@ -18,7 +19,8 @@ from helpers import assert_permutations, small_instance, to_acs
 pytestmark = pytest.mark.gpu
 
 GPU_OF = {("seq", O.DENSE): (O.SEQ, "seq"), ("sync", O.DENSE): (O.SYNC, "deferred"),
-          ("seq", O.SELECTIVE): (O.SEQ, "spm-seq")}
+          ("seq", O.SELECTIVE): (O.SEQ, "spm-seq"), ("sync", O.SELECTIVE): (O.SYNC, "spm-sync")}
+MODES = [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE), ("sync", O.SELECTIVE)]
 
 
 def pair(acs, orc, I, mode, memory, *, m, iters, seed=1, k=1, beta=3.0, q0=-1.0, cl=32, s=8,
@@ -58,14 +60,14 @@ def check_exact(st, routes, lens, state, cnt, best, o, memory):
     assert cnt["local_updates"] == o["local_updates"]
 
 
-@pytest.mark.parametrize("mode,memory", [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)])
+@pytest.mark.parametrize("mode,memory", MODES)
 def test_d198_bit_exact(acs, orc, gpu, mode, memory):
     I = O.load("d198")
     r = pair(acs, orc, I, mode, memory, m=40, iters=6)
     check_exact(*r, memory)
 
 
-@pytest.mark.parametrize("mode,memory", [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)])
+@pytest.mark.parametrize("mode,memory", MODES)
 @pytest.mark.parametrize("k", [2, 4])
 def test_update_period_bit_exact(acs, orc, gpu, mode, memory, k):
     I = O.load("a280")
@@ -73,7 +75,7 @@ def test_update_period_bit_exact(acs, orc, gpu, mode, memory, k):
     check_exact(*r, memory)
 
 
-@pytest.mark.parametrize("mode,memory", [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)])
+@pytest.mark.parametrize("mode,memory", MODES)
 def test_philox_bit_exact(acs, orc, gpu, mode, memory):
     I = O.load("lin318")
     r = pair(acs, orc, I, mode, memory, m=16, iters=4, rng="philox", seed=9)
@@ -81,19 +83,19 @@ def test_philox_bit_exact(acs, orc, gpu, mode, memory):
 
 
 @pytest.mark.parametrize("q0", [0.0, 0.5, 1.0])
-@pytest.mark.parametrize("mode", ["seq", "sync"])
-def test_q0_extremes_bit_exact(acs, orc, gpu, mode, q0):
+@pytest.mark.parametrize("mode,memory", [("seq", O.DENSE), ("sync", O.DENSE), ("sync", O.SELECTIVE)])
+def test_q0_extremes_bit_exact(acs, orc, gpu, mode, memory, q0):
     # q0 = 0 -> every candidate step is a roulette draw (exercises the
     # sequential-prefix warp roulette), q0 = 1 -> always greedy
     I = small_instance(150, seed=4)
-    r = pair(acs, orc, I, mode, O.DENSE, m=30, iters=3, q0=q0, seed=2)
-    check_exact(*r, O.DENSE)
+    r = pair(acs, orc, I, mode, memory, m=30, iters=3, q0=q0, seed=2)
+    check_exact(*r, memory)
 
 
 @pytest.mark.parametrize("beta,cl", [(0.0, 32), (1.0, 8), (2.0, 3), (5.0, 16)])
 def test_beta_and_cl_bit_exact(acs, orc, gpu, beta, cl):
     I = small_instance(120, seed=8)
-    for mode, memory in [("seq", O.DENSE), ("sync", O.DENSE), ("seq", O.SELECTIVE)]:
+    for mode, memory in MODES:
         r = pair(acs, orc, I, mode, memory, m=20, iters=3, beta=beta, cl=cl, seed=3)
         check_exact(*r, memory)
 
@@ -219,3 +221,12 @@ def test_sync_cooperative_scan_bit_exact(acs, orc, gpu):
     r = pair(acs, orc, I, "sync", O.DENSE, m=64, iters=2, seed=4, q0=0.3)
     check_exact(*r, O.DENSE)
     assert r[4]["fallback_full"] > 0
+
+
+@pytest.mark.parametrize("slots", [1, 2, 16])
+def test_spm_sync_slots_bit_exact(acs, orc, gpu, slots):
+    """SYNC x SELECTIVE with other record sizes, m = n (every record sees
+    convoys of inserts per step, applied in ant order)."""
+    I = O.load("d198")
+    r = pair(acs, orc, I, "sync", O.SELECTIVE, m=198, iters=3, seed=6, s=slots)
+    check_exact(*r, O.SELECTIVE)

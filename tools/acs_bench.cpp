@@ -7,7 +7,7 @@
 //                     --time-limit-ms T [options] [--out PREFIX]
 //
 // options: [--mode seq|sync|relaxed] [--memory dense|selective]
-//          [--variant atomic|deferred|relaxed|spm|seq|spm-seq] [--ants M]
+//          [--variant atomic|deferred|relaxed|spm|seq|spm-seq|spm-sync] [--ants M]
 //          [--iterations I | --budget B | --time-limit-ms T] [--update-period K] [--slots S]
 //          [--beta B] [--alpha A] [--rho R] [--phi R] [--q0 Q] [--cl CL] [--seed S] [--reps R]
 //          [--workers W] [--rng xoshiro|philox] [--device D] [--optima FILE] [--format csv|json]
@@ -90,6 +90,7 @@ void apply(acs::AcsParams &p, const std::string &k, const std::string &v) {
         p.variant = v == "atomic" ? acs::Variant::kAtomic : v == "deferred" ? acs::Variant::kDeferred
                   : v == "relaxed" ? acs::Variant::kRelaxed : v == "spm" ? acs::Variant::kSpm
                   : v == "seq" ? acs::Variant::kSeq : v == "spm-seq" ? acs::Variant::kSpmSeq
+                  : v == "spm-sync" ? acs::Variant::kSpmSync
                   : v == "auto" ? acs::Variant::kAuto
                   : throw std::invalid_argument("unknown variant " + v);
     } else if (k == "rng") {
