@@ -119,7 +119,7 @@ def algorithmic_bytes_per_tour(n: int, L: int, k: int, variant: str, slots: int 
     The fallback term F is added from the device counter by the caller."""
     S = 8
     upd = -(-n // k)
-    if variant in ("spm", "spm-seq"):
+    if variant in ("spm", "spm-seq", "spm-sync"):
         return n * (L * (4 + S) + slots * (4 + S) + 8) + upd * 2 * (slots * 4 + S + 4)
     return n * (L * (4 + S) + 4) + upd * 4 * S
 
@@ -170,8 +170,9 @@ def run_reference(args):
     I = O.load(args.instance)
     m = args.ants or I.n
     threads = os.cpu_count() or 1
-    mode = O.SEQ if args.variant in ("seq", "spm-seq") else (O.SYNC if args.variant == "deferred" else O.RELAXED)
-    memory = O.SELECTIVE if args.variant in ("spm", "spm-seq") else O.DENSE
+    mode = O.SEQ if args.variant in ("seq", "spm-seq") else (
+        O.SYNC if args.variant in ("deferred", "spm-sync") else O.RELAXED)
+    memory = O.SELECTIVE if args.variant in ("spm", "spm-seq", "spm-sync") else O.DENSE
     consistent = 1 if args.variant == "atomic" else 0
     orc = O.Oracle()
     # Each step is one ACS iteration of a bounded sample of the colony
