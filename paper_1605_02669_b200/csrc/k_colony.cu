@@ -763,7 +763,9 @@ struct SpmRec {
     }
 };
 
-template <int S, class RNG>
+// kLean: k = 1 and 32-slot lists (as the dense kernel): no period counter,
+// no list-length tests on the step path
+template <int S, class RNG, bool kLean = false>
 __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -799,11 +801,11 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
             }
             const double tau_lane = rec.lookup(el.x & kIdMask, C.tau_min);
             Step st;
-            select_step(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
+            select_step<false, kLean>(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
                         [&](uint32_t v, bool act) { return rec.lookup(act ? v : kEmpty, C.tau_min); }, st);
             wc.count(st.kind, n - t);
             el = __ldg(C.rows + static_cast<size_t>(st.v) * 32 + lane);  // next row first
-            pending = (++kc == C.k);
+            pending = kLean || (++kc == C.k);
             if (pending) {
                 kc = 0;
                 ++wc.updates;
@@ -1551,7 +1553,10 @@ static void launch_spm_rng(const DevInstance &I, const DevColony &C, bool one_wa
         case 1: launch_tour_kernel(k_construct_spm<1, RNG>, I, C, one_warp, s); break;
         case 2: launch_tour_kernel(k_construct_spm<2, RNG>, I, C, one_warp, s); break;
         case 4: launch_tour_kernel(k_construct_spm<4, RNG>, I, C, one_warp, s); break;
-        case 8: launch_tour_kernel(k_construct_spm<8, RNG>, I, C, one_warp, s); break;
+        case 8:
+            if (C.k == 1 && C.L == 32 && !one_warp) launch_tour_kernel(k_construct_spm<8, RNG, true>, I, C, false, s);
+            else launch_tour_kernel(k_construct_spm<8, RNG>, I, C, one_warp, s);
+            break;
         default: launch_tour_kernel(k_construct_spm<16, RNG>, I, C, one_warp, s); break;
     }
 }
