@@ -151,9 +151,9 @@ def cpu_baseline_seq(name: str, m: int, k: int):
     """oracle SEQ (ACS-SEQ restated) on one host core, bounded sample."""
     import oracle as O
     I = O.load(name)
-    # bounded sample (~5-20 s of one core): 3 full iterations up to pr2392,
+    # bounded sample (~10-20 s of one core): 7 full iterations up to pr2392,
     # one iteration of a 1000-ant colony beyond
-    iters, m_s = (3, m) if I.n <= 4096 else (1, min(m, 1000))
+    iters, m_s = (7, m) if I.n <= 4096 else (1, min(m, 1000))
     o = O.Oracle().run(I, m=m_s, iterations=iters, seed=0, mode=O.SEQ, k=k, want_routes=False)
     tps = m_s * iters / (o["loop_ms"] / 1e3)
     return {"value": round(tps, 1), "unit": "tours/s", "cores": 1, "kind": "port",
