@@ -633,7 +633,25 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
 // arrays; 4 counters per thread step, skipping untouched words.
 __global__ void k_fold_counts(DevColony C, size_t dense_count, size_t cand_count) {
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < dense_count; i += stride) {
+    const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // dense counters as 16-byte vectors (4 per load): the sweep is a pure
+    // HBM/L2 read of n^2 x 4 B; tau is touched only where a count is pending
+    const size_t q4 = dense_count / 4;
+    const uint4 *cnt4 = reinterpret_cast<const uint4 *>(C.cnt);
+    for (size_t q = t0; q < q4; q += stride) {
+        const uint4 c = cnt4[q];
+        if ((c.x | c.y | c.z | c.w) == 0u) continue;
+        const uint32_t cs[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (cs[j]) {
+                const size_t i = 4 * q + j;
+                C.tau[i] = trail_value(C.tau[i], cs[j], C, C.pw_lo, C.pw_hi);
+                C.cnt[i] = 0;
+            }
+        }
+    }
+    for (size_t i = 4 * q4 + t0; i < dense_count; i += stride) {
         const uint32_t c = C.cnt[i];
         if (c) {
             C.tau[i] = trail_value(C.tau[i], c, C, C.pw_lo, C.pw_hi);
