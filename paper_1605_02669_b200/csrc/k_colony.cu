@@ -1541,14 +1541,24 @@ template <int kMode, class RNG, bool kLean>
 static void launch_dense_t(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw) {
     auto narrow = k_construct_dense<kMode, RNG, kMaxRegs, kLean>;
     if (!one_warp) {
-        int dev = 0, sms = 0, per_sm = 0;
+        // The narrow-vs-wide decision (occupancy query) is made once per
+        // (device, shared memory, m) and remembered per host thread: it costs
+        // microseconds of host time between the step's start event and the
+        // kernel, which small instances (d198: 0.17 ms per step) would see.
+        struct Memo { int dev = -1; size_t smem = 0; uint32_t m = 0; bool wide = false; };
+        static thread_local Memo memo;
+        int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const size_t smem = construct_smem(I, C, kBlock / 32, pw);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, narrow, kBlock, smem);
-        if (static_cast<uint64_t>(per_sm) * sms * (kBlock / 32) < C.m) {
+        if (memo.dev != dev || memo.smem != smem || memo.m != C.m) {
+            int sms = 0, per_sm = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, narrow, kBlock, smem);
+            memo = Memo{dev, smem, C.m, static_cast<uint64_t>(per_sm) * sms * (kBlock / 32) < C.m};
+        }
+        if (memo.wide) {
             launch_tour_kernel(k_construct_dense<kMode, RNG, kWideRegs, kLean>, I, C, false, s, pw);
             return;
         }
