@@ -1645,9 +1645,11 @@ int launch_deferred(int rng, const DevInstance &I, const DevColony &C, const Dev
 void launch_epilogue(bool spm, bool fold, const DevInstance &I, const DevColony &C,
                      const DevBest &B, uint32_t slot, cudaStream_t s) {
     k_best<<<1, 1024, 0, s>>>(C, B, I.n, slot);
-    if (fold)
-        k_fold_counts<<<148 * 8, 256, 0, s>>>(C, static_cast<size_t>(I.n) * I.n,
-                                              static_cast<size_t>(I.n) * 32);
+    if (fold) {  // grid sized to the counters (4 per thread), at most 8 CTAs per SM
+        const size_t dense = static_cast<size_t>(I.n) * I.n;
+        k_fold_counts<<<std::min<size_t>(148 * 8, blocks_for(dense / 4 + 1, 256)), 256, 0, s>>>(
+            C, dense, static_cast<size_t>(I.n) * 32);
+    }
     if (spm) k_global_spm<<<blocks_for(I.n, 256), 256, 0, s>>>(I, C, B);
     else k_global_dense<<<blocks_for(I.n, 8), 256, 0, s>>>(I, C, B);
 }
