@@ -10,13 +10,15 @@ mkdir -p gpurun_out
 S=${SEEDS:-10}
 S0=${SEED0:-0}
 TAG=${TAG:-qb}
+M=${ANTS:-256}
+VARS=${VARS:-relaxed spm}
 for spec in ${SPECS:-nrw1379:1379 pr2392:2392}; do
   inst=${spec%%:*}; n=${spec##*:}
   for k in ${KS:-1 2 4 8 16}; do
-    python tools/quality.py --instances $inst --variants relaxed spm --ants 256 --k $k --seeds $S --seed0 $S0 \
-      --iterations $((1000 * n / 256)) --out gpurun_out/${TAG}_${inst}_m256_k$k.json
+    python tools/quality.py --instances $inst --variants $VARS --ants $M --k $k --seeds $S --seed0 $S0 \
+      --iterations $((1000 * n / M)) --out gpurun_out/${TAG}_${inst}_m${M}_k$k.json
   done
-  for m in ${MS:-128 512 1024}; do
+  for m in ${MS-128 512 1024}; do
     python tools/quality.py --instances $inst --variants relaxed --ants $m --k 1 --seeds $S --seed0 $S0 \
       --iterations $((1000 * n / m)) --out gpurun_out/${TAG}_${inst}_m${m}_k1.json
   done
