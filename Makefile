@@ -20,7 +20,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -warn-spill
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -ffp-contract=off -I include \
             -I /usr/local/cuda/include
 
-CU_SRCS := $(SRC)/k_setup.cu $(SRC)/k_colony.cu $(SRC)/capi.cu
+CU_SRCS := $(SRC)/k_setup.cu $(SRC)/k_colony.cu $(SRC)/k_micro.cu $(SRC)/capi.cu
 CXX_SRCS := $(SRC)/instance.cpp $(SRC)/solver.cpp $(SRC)/stats.cpp
 CU_OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS))
 CXX_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CXX_SRCS))
@@ -62,7 +62,8 @@ ab:
 	$(NVCC) $(NVFLAGS) $(DEFS) -c $(or $(COLONY),$(SRC)/k_colony.cu) -o build/obj_$(V)/k_colony.o
 	$(NVCC) $(NVFLAGS) $(DEFS) -c $(SRC)/k_setup.cu -o build/obj_$(V)/k_setup.o
 	$(NVCC) $(NVFLAGS) $(DEFS) -c $(SRC)/capi.cu -o build/obj_$(V)/capi.o
+	$(NVCC) $(NVFLAGS) $(DEFS) -c $(SRC)/k_micro.cu -o build/obj_$(V)/k_micro.o
 	$(NVCC) $(ARCH) -shared -o $(PKG)/libacs_b200_$(V).so build/obj_$(V)/k_colony.o build/obj_$(V)/k_setup.o \
-	  build/obj_$(V)/capi.o $(CXX_OBJS) -lz -ldl
+	  build/obj_$(V)/k_micro.o build/obj_$(V)/capi.o $(CXX_OBJS) -lz -ldl
 
 .PHONY: ab

@@ -124,6 +124,15 @@ def algorithmic_bytes_per_tour(n: int, L: int, k: int, variant: str, slots: int 
     return n * (L * (4 + S) + 4) + upd * 4 * S
 
 
+def resident_ants(P, device: int, m: int) -> int:
+    """Ants constructing at once (one warp each): 20 per SM with the 96-register
+    build (5 warps per sub-partition), 28 with the 72-register build the
+    launcher picks for colonies larger than one wave (k_colony.cu kWideRegs)."""
+    import torch
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    return sms * 20 if m <= sms * 20 else sms * 28
+
+
 def measured_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -162,7 +171,12 @@ def cpu_baseline_seq(name: str, m: int, k: int):
 
 
 def run_reference(args):
-    """--impl reference: the CPU port of the reference path on all host threads."""
+    """--impl reference: the reference's path on the host cores, SAME workload
+    as the GPU arm: one persistent colony of m ants on the same instance, the
+    same variant semantics (SPEC mode x memory x contract) and the same per-ant
+    RNG engine, W warm-up and K timed iterations of that one colony.  The
+    oracle (oracle/acs_oracle.c, the CPU restatement of the reference path,
+    OpenMP over all host threads) times every iteration itself (iter_ms)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
@@ -174,33 +188,27 @@ def run_reference(args):
         O.SYNC if args.variant in ("deferred", "spm-sync") else O.RELAXED)
     memory = O.SELECTIVE if args.variant in ("spm", "spm-seq", "spm-sync") else O.DENSE
     consistent = 1 if args.variant == "atomic" else 0
-    orc = O.Oracle()
-    # Each step is one ACS iteration of a bounded sample of the colony
-    # (min(m, 1024) ants) so that --steps K --warmup W stays within minutes;
-    # the metric is per tour, so the sample does not bias it.  The oracle keeps
-    # no state across calls: every step is a fresh single-iteration colony.
-    m_step = min(m, 1024)
-    for w in range(args.warmup):
-        orc.run(I, m=m_step, iterations=1, seed=args.seed + 1000 + w, mode=mode, memory=memory,
-                consistent=consistent, threads=threads, k=args.k, want_routes=False)
-    loop_ms = []
-    for st in range(args.steps):
-        o = orc.run(I, m=m_step, iterations=1, seed=args.seed + st, mode=mode, memory=memory,
-                    consistent=consistent, threads=threads, k=args.k, want_routes=False)
-        loop_ms.append(o["loop_ms"])
-    total_s = sum(loop_ms) / 1e3
-    value = m_step * args.steps / total_s
+    rng = rng_for(args.variant, args.rng)
+    o = O.Oracle().run(I, m=m, iterations=args.warmup + args.steps, seed=args.seed, mode=mode,
+                       memory=memory, consistent=consistent, threads=threads, k=args.k,
+                       rng=O.PHILOX if rng == "philox" else O.XOSHIRO, want_routes=False)
+    timed_ms = float(o["iter_ms"][args.warmup:].sum())
+    value = m * args.steps / (timed_ms / 1e3)
+    cfg = bench_config(args, I.n, m, world)
+    cfg["reference_mode"] = {"mode": ["seq", "sync", "relaxed"][mode], "memory": ["dense", "selective"][memory],
+                             "consistent": consistent}
+    cpu = host_cpu_model()
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "tours/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(sum(loop_ms) / args.steps * m / m_step, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(timed_ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": data_desc(args.instance),
-        "config": {"workload": f"{args.instance} ACS, {m} ants, cl=32, k={args.k}, {args.variant}",
-                   "variant": args.variant, "mode": ["seq", "sync", "relaxed"][mode],
-                   "memory": ["dense", "selective"][memory], "consistent": consistent},
+        "config": cfg,
         "cpu_baseline": {"value": round(value, 1), "unit": "tours/s", "cores": threads, "kind": "port",
-                         "sample": f"oracle/acs_oracle.c OpenMP on {threads} host threads, "
-                                   f"{args.steps} iterations x {m_step} of {m} ants per step"},
+                         "cpu": cpu,
+                         "sample": f"oracle/acs_oracle.c (OpenMP, {threads} threads on {cpu}): one persistent "
+                                   f"{m}-ant colony, {args.warmup} warm-up + {args.steps} timed iterations "
+                                   f"(per-iteration wall time), best L_gb {int(o['best_len'])}"},
         "e2e": {"value": round(value, 1), "unit": "tours/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -211,6 +219,34 @@ def rng_for(variant: str, rng: str) -> str:
     if rng != "auto":
         return rng
     return "philox" if variant in ("atomic", "relaxed") else "xoshiro"
+
+
+def default_q0(n: int) -> float:
+    """SPEC D6 default q0 = (n - 20) / n (capi.cu default_q0)."""
+    return 0.0 if n <= 20 else (n - 20) / n
+
+
+def bench_config(args, n: int, m: int, world: int, exchange=None) -> dict:
+    """The workload both arms run (the reference arm prints the same dict)."""
+    return {"workload": f"{args.instance} ACS, {m} ants, cl=32, k={args.k}, {args.variant} dense"
+            if args.variant not in ("spm", "spm-seq", "spm-sync") else f"{args.instance} ACS-SPM, {m} ants, s=8",
+            "instance": args.instance, "n": n, "ants_per_gpu": m, "variant": args.variant,
+            "cl": 32, "k": args.k, "beta": 3.0, "alpha": 0.2, "rho": 0.01,
+            "q0": round(default_q0(n), 6), "rng": rng_for(args.variant, args.rng),
+            "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": f"island x{world}" if world > 1 else "single colony",
+            "exchange_every": args.exchange_every if world > 1 else None, "exchange": exchange}
+
+
+def host_cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def main():
@@ -233,6 +269,9 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
+        if not shared:  # NCCL's own init lines carry the communicator size (nRanks)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if shared:
             dist.init_process_group("gloo")
         else:
@@ -254,6 +293,8 @@ def main():
             dist.broadcast_object_list(uid, src=0)
             col.island_init(uid[0], world, rank)
             exchange = "device (NCCL inside libacs_b200)"
+            print(f"[acs] island NCCL communicator: rank {rank} of nranks {world} on cuda:{local}",
+                  file=sys.stderr, flush=True)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     # our kernels per iteration: construction (1 launch; deferred = 1 cooperative
@@ -296,30 +337,42 @@ def main():
     value = world * m * args.steps / (total_ms / 1e3)
     order, best_len = col.best()
 
-    # roofline of the dominant kernel (construction): algorithmic bytes / launch time
+    # Roofline of the dominant kernel (construction).  Its working set is
+    # L2-resident: the bound is the L2, with the L2 read
+    # bandwidth measured in this run as the peak; the HBM figure is kept
+    # alongside.  Algorithmic bytes = the per-tour term x m
+    # + F, the fallback term, reported separately: F counts n - t nodes x
+    # 12 B for every fallback step as if it scanned all unvisited nodes,
+    # which the pruned pass mostly does not.
     fb_elems = c1.get("fallback_elems", 0) - c0.get("fallback_elems", 0)
     B_tour = algorithmic_bytes_per_tour(inst.n, col.info.list_len, args.k, args.variant)
-    alg_bytes_launch = B_tour * m + fb_elems * 12 / max(args.steps, 1)
+    F_launch = fb_elems * 12 / max(args.steps, 1)
+    alg_bytes_launch = B_tour * m + F_launch
     construct_s = construct_ms / 1e3 / args.steps
     peaks, src = measured_peaks()
     achieved = alg_bytes_launch / construct_s / 1e9
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic(args.variant),
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
-                "kernel": "k_construct_dense" if args.variant != "spm" else "k_construct_spm",
-                "construct_ms_per_launch": round(construct_s * 1e3, 4),
-                "bytes_per_tour": B_tour,
-                "note": "latency-bound dependent-load chain; L2-resident working set"}
-    # the working set is L2-resident: the same bytes against the
-    # measured L2 read bandwidth, and the ncu L2 read traffic per launch
     l2_gbs = P._native.l2_read_bandwidth(local, 48 << 20)
     rec = ncu_record(args.variant)
     sectors = rec.get("lts__t_sectors_srcunit_tex_op_read.sum")
-    roofline["l2"] = {"peak": round(l2_gbs, 1), "unit": "GB/s", "achieved": round(achieved, 1),
-                      "frac": round(achieved / l2_gbs, 4),
-                      "peak_source": "acs_gpu_l2_read_bandwidth: ld.global.cg stream over a 48 MiB "
-                                     "L2-resident buffer, measured in this run",
-                      "ncu_l2_read_bytes_per_launch": sectors * 32 if sectors else None}
+    l2_read = sectors * 32 if sectors else None
+    roofline = {"bound": "l2", "achieved": round(achieved, 1), "peak": round(l2_gbs, 1), "unit": "GB/s",
+                "frac": round(achieved / l2_gbs, 4), "traffic": ncu_traffic(args.variant),
+                "traffic_note": "dram bytes per launch (ncu --set full, committed capture); the working set "
+                                "is L2-resident, so DRAM traffic is the cold fill only",
+                "peak_source": "acs_gpu_l2_read_bandwidth: ld.global.cg stream over a 48 MiB L2-resident "
+                               "buffer, measured in this run",
+                "kernel": "k_construct_dense" if args.variant not in ("spm",) else "k_construct_spm",
+                "construct_ms_per_launch": round(construct_s * 1e3, 4),
+                "bytes_per_tour": B_tour,
+                "algorithmic_bytes_per_launch": round(alg_bytes_launch),
+                "fallback_bytes_per_launch": round(F_launch),
+                "l2_read_bytes_per_launch": l2_read,
+                "l2_traffic_ratio": round(l2_read / (B_tour * m), 3) if l2_read else None,
+                "l2_traffic_ratio_note": "ncu L2 read bytes per launch / the per-tour algorithmic bytes x m "
+                                         "(without F): >1 means bytes read that the algorithm does not need",
+                "hbm": {"peak": peaks["hbm_gbs"], "frac": round(achieved / peaks["hbm_gbs"], 4),
+                        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"},
+                "note": "latency-bound dependent-load chain; L2-resident working set"}
 
     # The construction loop is a dependent chain per ant, so its practical
     # ceiling is instruction issue (one warp instruction per SM sub-partition
@@ -333,13 +386,25 @@ def main():
         roofline["issue"] = {"achieved": round(n_inst / construct_s / 1e12, 4), "peak": round(peak_ips / 1e12, 4),
                              "unit": "T warp-inst/s", "frac": round(n_inst / construct_s / peak_ips, 4),
                              "inst_per_launch": n_inst,
+                             "inst_per_step": round(n_inst / (m * (inst.n - 1)), 1),
                              "source": "ncu --set full 'Executed Instructions' of this variant's construct kernel "
                                        "(profiles/ncu_construct_summary.json) / this run's launch time; peak = "
                                        "4 schedulers x SMs x median SM clock under load"}
-    # Latency bound: every ant is a chain of n-1 dependent steps, so no colony
-    # can construct faster than ONE isolated ant's tour.  A 128-ant colony
-    # (< 1 ant per SM, no issue contention) of the same variant measures that
-    # chain in this run; frac = its construct time / the full colony's.
+    # Latency floor (hardware, not this kernel): acs_gpu_l2_latency measures
+    # the L2 load-to-use latency (pointer chase) and one warp's MINIMAL
+    # selection step over L2-resident rows (row + trail load, visited test,
+    # score, exact argmax, next row = the winner's).  Every ant is a chain of
+    # n - 1 such steps, so ns per step of the colony = launch time / (n - 1)
+    # cannot go below floor_ns_per_step.
+    load_ns, step_ns = P._native.l2_latency(local, 48 << 20)
+    ach_step_ns = construct_s * 1e9 / ((inst.n - 1) * max(1, -(-m // resident_ants(P, local, m))))
+    roofline["latency"] = {"floor_ns_per_step": round(step_ns, 1), "l2_load_ns": round(load_ns, 1),
+                           "achieved_ns_per_step": round(ach_step_ns, 1),
+                           "frac": round(step_ns / ach_step_ns, 4),
+                           "source": "acs_gpu_l2_latency in this run: L2 pointer chase (ld.global.cg, 48 MiB) and "
+                                     "one warp's minimal selection step over L2-resident rows; achieved = launch "
+                                     "time / (n - 1) steps / waves"}
+    # the isolated ant of THIS kernel (128-ant colony, < 1 ant per SM)
     p_lat = P.AcsParams(variant=args.variant, m=128, k=args.k, seed=args.seed, rng=rng_for(args.variant, args.rng))
     with P.Colony(inst, p_lat, device=local) as lc:
         lc.iterate(2)
@@ -350,10 +415,11 @@ def main():
             lc.iterate(1)
             lat.append(lc.last_timing()[1])
     lat_ms = statistics.median(lat)
-    roofline["latency"] = {"bound_ms": round(lat_ms, 4), "achieved_ms": round(construct_s * 1e3, 4),
-                           "frac": round(lat_ms / (construct_s * 1e3), 4),
-                           "source": "construct time of a 128-ant colony (same variant, < 1 ant per SM: the "
-                                     "isolated dependent chain of n-1 steps), median of 5, measured in this run"}
+    roofline["latency"]["isolated_ant"] = {
+        "ms": round(lat_ms, 4), "ns_per_step": round(lat_ms * 1e6 / (inst.n - 1), 1),
+        "frac_colony": round(lat_ms / (construct_s * 1e3), 4),
+        "source": "construct time of a 128-ant colony of the same kernel, median of 5: the colony's time "
+                  "over one ant's chain (issue contention)"}
     col.close()
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tours/s", "n_gpus": world,
@@ -362,13 +428,7 @@ def main():
         "vs_baseline": round(value / PAPER_ACS_GPU_PR2392, 2) if args.instance == "pr2392" and args.variant == "atomic" else None,
         "vs_baseline_ref": "paper ACS-GPU (atomic) pr2392 4942 tours/s on GK104 (BASELINE.md, PAPER.md:920)",
         "dtype": "f64", "data": data_desc(args.instance),
-        "config": {"workload": f"{args.instance} ACS, {m} ants, cl=32, k={args.k}, {args.variant} dense"
-                   if args.variant != "spm" else f"{args.instance} ACS-SPM, {m} ants, s=8",
-                   "instance": args.instance, "n": inst.n, "ants_per_gpu": m, "variant": args.variant,
-                   "cl": 32, "k": args.k, "beta": 3.0, "alpha": 0.2, "rho": 0.01,
-                   "q0": round(col.info.q0, 6), "rng": rng_for(args.variant, args.rng), "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": f"island x{world}" if world > 1 else "single colony",
-                   "exchange_every": args.exchange_every if world > 1 else None, "exchange": exchange},
+        "config": bench_config(args, inst.n, m, world, exchange),
         "roofline": roofline,
         "gpu_launches": launches_per_iter * args.steps,
         "clocks": clk.summary(),
@@ -422,9 +482,13 @@ def e2e(P, inst, params, args, world, dist=None, device=0, shared=False):
     coordinates H2D, setup kernels), then every step one acs_gpu_iterate(ctx,
     1, &stats) with that step's result (iteration best, L_gb: 24 B) read back
     to the host, then the best tour D2H and destroy -- all inside the timed
-    region.  Every rank runs its own colony at the same time; the whole-job
-    value uses the max wall time over ranks.  Repeated 3 times (host wall
-    clocks on the box jitter by tens of ms); the median is reported."""
+    region.  At N > 1 every rank runs its own colony at the same time and the
+    colonies exchange their best every --exchange-every steps inside the timed
+    region (acs_gpu_island_exchange over NCCL; host exchange over gloo when
+    ranks share a GPU); the NCCL communicator setup (acs_gpu_island_init, the
+    analogue of init_process_group) is excluded from the wall time.  The
+    whole-job value uses the max wall time over ranks.  Repeated 3 times (host
+    wall clocks on the box jitter by tens of ms); the median is reported."""
     import ctypes as C
     import numpy as np
     from paper_1605_02669_b200 import _native as N
@@ -434,26 +498,46 @@ def e2e(P, inst, params, args, world, dist=None, device=0, shared=False):
     order = np.empty(inst.n, np.uint32)
     bl = C.c_int64()
     stat = N.IterStats()
+    gbl = C.c_int64()
     lib = N.lib()
+    nccl = world > 1 and not shared
+    exchanges = [0]
 
     def one(k):
+        if nccl:  # the unique id travels over the process group, before the clock starts
+            uid = [P.Colony.nccl_unique_id() if dist.get_rank() == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ubuf = C.create_string_buffer(uid[0], 128)
         h = C.c_void_p()
+        t0 = time.perf_counter()
         N.check(lib.acs_gpu_create(C.byref(d), C.byref(p), device, C.byref(h)), "acs_gpu_create")
+        excluded = 0.0
         try:
-            for _ in range(k):
+            if nccl:
+                ti = time.perf_counter()
+                N.check(lib.acs_gpu_island_init(h, ubuf, world, dist.get_rank()), "acs_gpu_island_init")
+                excluded = time.perf_counter() - ti
+            n_ex = 0
+            for i in range(k):
                 N.check(lib.acs_gpu_iterate(h, 1, C.byref(stat)), "acs_gpu_iterate")
+                if world > 1 and (i + 1) % args.exchange_every == 0:
+                    n_ex += 1
+                    if nccl:
+                        N.check(lib.acs_gpu_island_exchange(h, C.byref(gbl)), "acs_gpu_island_exchange")
+                    else:
+                        P.island.exchange_host(_CtxView(lib, h, inst.n), dist)
             N.check(lib.acs_gpu_get_best(h, order.ctypes.data_as(C.c_void_p), C.byref(bl)), "acs_gpu_get_best")
+            exchanges[0] = n_ex
         finally:
             lib.acs_gpu_destroy(h)
+        return time.perf_counter() - t0 - excluded
 
     one(1)  # untimed: lazy CUDA module loading of the setup kernels
     walls = []
     for _ in range(3):
         if dist:
             dist.barrier()
-        t0 = time.perf_counter()
-        one(K)
-        dt = time.perf_counter() - t0
+        dt = one(K)
         if dist:
             import torch
             t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else f"cuda:{device}")
@@ -462,13 +546,41 @@ def e2e(P, inst, params, args, world, dist=None, device=0, shared=False):
         walls.append(dt)
     dt = statistics.median(walls)
     m = p.ants
+    ex_bytes = exchanges[0] * (8 if nccl else 8 + 4 * inst.n) / K  # L_gb read back per exchange (host path: + tour)
     return {"value": round(world * m * K / dt, 1), "unit": "tours/s",
             "h2d_bytes_per_step": round(2 * 8 * inst.n / K, 1),
-            "d2h_bytes_per_step": round(C.sizeof(N.IterStats) + (4 * inst.n + 8) / K, 1),
-            "api": f"acs_gpu_create + K x acs_gpu_iterate(ctx, 1, &stats) (per-step result D2H) + "
-                   f"acs_gpu_get_best + acs_gpu_destroy, host buffers, on each of {world} rank(s); "
+            "d2h_bytes_per_step": round(C.sizeof(N.IterStats) + (4 * inst.n + 8) / K + ex_bytes, 1),
+            "api": f"acs_gpu_create + K x acs_gpu_iterate(ctx, 1, &stats) (per-step result D2H)"
+                   + (f" + island exchange every {args.exchange_every} steps ({exchanges[0]} per run, "
+                      + ("acs_gpu_island_exchange over NCCL" if nccl else "host exchange over gloo") + ")"
+                      if world > 1 else "")
+                   + f" + acs_gpu_get_best + acs_gpu_destroy, host buffers, on each of {world} rank(s); "
                    f"max wall over ranks, median of 3 runs",
+            "nccl_comm_nranks": world if nccl else None,
             "wall_s": round(dt, 4), "wall_s_runs": [round(w, 4) for w in walls]}
+
+
+class _CtxView:
+    """best()/set_best() of a raw C-ABI context, for island.exchange_host."""
+
+    def __init__(self, lib, h, n):
+        self.lib, self.h, self.n = lib, h, n
+
+    def best(self):
+        import ctypes as C
+        import numpy as np
+        from paper_1605_02669_b200 import _native as N
+        order = np.empty(self.n, np.uint32)
+        ln = C.c_int64()
+        N.check(self.lib.acs_gpu_get_best(self.h, order.ctypes.data_as(C.c_void_p), C.byref(ln)), "get_best")
+        return order, ln.value
+
+    def set_best(self, order, length):
+        import ctypes as C
+        import numpy as np
+        from paper_1605_02669_b200 import _native as N
+        order = np.ascontiguousarray(order, np.uint32)
+        N.check(self.lib.acs_gpu_set_best(self.h, order.ctypes.data_as(C.c_void_p), int(length)), "set_best")
 
 
 if __name__ == "__main__":

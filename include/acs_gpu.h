@@ -27,7 +27,8 @@
 extern "C" {
 #endif
 
-#define ACS_GPU_ABI_VERSION 3  /* 2: acs_counters.fallback_full, acs_random_instance; 3: ACS_VARIANT_SPM_SYNC */
+#define ACS_GPU_ABI_VERSION 4  /* 2: acs_counters.fallback_full, acs_random_instance; 3: ACS_VARIANT_SPM_SYNC;
+                                  4: acs_gpu_island_exchange_local, acs_gpu_l2_latency, 16-bit island ranks */
 
 /* status codes */
 #define ACS_OK 0
@@ -126,6 +127,12 @@ int acs_rank_sum_test(const double *xs, uint32_t nx, const double *ys, uint32_t 
 /* diagnostic: L2 read bandwidth (GB/s) streaming over an L2-resident buffer of
  * `bytes` (the roofline denominator of the L2-resident construction working set) */
 int acs_gpu_l2_read_bandwidth(int device, uint64_t bytes, double *gbs);
+/* diagnostic: absolute per-step floors of the construction chain over an
+ * L2-resident buffer of `bytes` (>= 4 MiB; 48 MiB is L2- but not L1-resident):
+ *   *load_ns  L2 load-to-use latency (one-thread pointer chase, ld.global.cg)
+ *   *step_ns  one warp's minimal selection step: 512 B row + 256 B trail load,
+ *             visited test, score, exact warp argmax, next row = the winner's */
+int acs_gpu_l2_latency(int device, uint64_t bytes, double *load_ns, double *step_ns);
 
 /* ---- stateless device ops (setup path) ----
  * replaces TspInstance ctor's dist_table_ (tsp_instance.cpp:23-47) */
@@ -184,6 +191,12 @@ int acs_gpu_island_init(acs_gpu_ctx *ctx, const void *unique_id, int nranks, int
 /* min-allreduce of (L_gb, rank) then broadcast of the winner's tour; every
  * colony adopts it if strictly better.  Device-side, no host round trip. */
 int acs_gpu_island_exchange(acs_gpu_ctx *ctx, int64_t *global_best_len);
+/* islands within one GPU: the same exchange (same pack / mask / adopt kernels,
+ * ties to the lowest index, strictly-better adoption) among `count` colonies
+ * of this process on one device, with the two all-reduces done as device
+ * reductions; ctxs[i] plays rank i.  *global_best_len = INT64_MAX when no
+ * colony has a tour yet. */
+int acs_gpu_island_exchange_local(acs_gpu_ctx *const *ctxs, int count, int64_t *global_best_len);
 
 #ifdef __cplusplus
 }

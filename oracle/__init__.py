@@ -131,7 +131,7 @@ class OrcReport(C.Structure):
                 ("local_updates", C.c_uint64), ("hits", C.c_uint64), ("misses", C.c_uint64),
                 ("fallback_steps", C.c_uint64), ("greedy_steps", C.c_uint64),
                 ("roulette_steps", C.c_uint64), ("tau0", C.c_double), ("nn_len", C.c_int64),
-                ("elapsed_ms", C.c_double), ("loop_ms", C.c_double)]
+                ("elapsed_ms", C.c_double), ("loop_ms", C.c_double), ("iter_ms", C.c_void_p)]
 
 
 def _ptr(a):
@@ -240,7 +240,8 @@ class Oracle:
                       consistent, rng, threads)
         out = dict(best_tour=np.zeros(n, np.uint32), trace=np.zeros(iterations, np.int64),
                    iter_best_len=np.zeros(iterations, np.int64),
-                   iter_best_ant=np.zeros(iterations, np.uint32))
+                   iter_best_ant=np.zeros(iterations, np.uint32),
+                   iter_ms=np.zeros(iterations, np.float64))
         if want_routes:
             out["routes"] = np.zeros((m, n), np.uint32)
             out["lengths"] = np.zeros(m, np.int64)
@@ -252,7 +253,7 @@ class Oracle:
             out["spm_tail"] = np.zeros(n, np.uint32)
         rep = OrcReport()
         for key in ("best_tour", "trace", "iter_best_len", "iter_best_ant", "routes", "lengths",
-                    "tau", "spm_ids", "spm_vals", "spm_tail"):
+                    "tau", "spm_ids", "spm_vals", "spm_tail", "iter_ms"):
             setattr(rep, key, _ptr(out.get(key)))
         rc = self.lib.orc_run(n, I.type, I.xs, I.ys, C.byref(p), C.byref(rep))
         if rc != 0:

@@ -583,6 +583,7 @@ int orc_run(uint32_t n, int type, const double *xs, const double *ys,
 
     const double t_loop = now_ms();
     for (uint64_t it = 0; it < p->iterations; ++it) {
+        const double t_it = now_ms();
         if (p->mode == ORC_SEQ) { /* ant-major, immediate updates */
             ant_t *A = &ants[0];
             for (uint32_t a = 0; a < m; ++a) {
@@ -640,6 +641,7 @@ int orc_run(uint32_t n, int type, const double *xs, const double *ys,
         if (rep->trace) rep->trace[it] = gb_len;
         if (rep->iter_best_len) rep->iter_best_len[it] = lens[ib];
         if (rep->iter_best_ant) rep->iter_best_ant[it] = ib;
+        if (rep->iter_ms) rep->iter_ms[it] = now_ms() - t_it;
     }
     rep->loop_ms = now_ms() - t_loop;
     for (uint32_t i = 0; i < n_states; ++i) {

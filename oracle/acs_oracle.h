@@ -106,6 +106,7 @@ typedef struct {
     int64_t nn_len;
     double elapsed_ms;        /* whole call incl. setup */
     double loop_ms;           /* iteration loop only (construct+eval+best+global) */
+    double *iter_ms;          /* [iterations] wall time of each iteration, or NULL */
 } orc_report;
 
 int orc_run(uint32_t n, int type, const double *xs, const double *ys,

@@ -69,6 +69,7 @@ SIGNATURES = {
                                    _u32, C.c_char_p, C.c_size_t]),
     "acs_random_instance": (C.c_int, [_u32, _u64, _u32, _P, _P]),
     "acs_gpu_l2_read_bandwidth": (C.c_int, [C.c_int, _u64, C.POINTER(_f64)]),
+    "acs_gpu_l2_latency": (C.c_int, [C.c_int, _u64, C.POINTER(_f64), C.POINTER(_f64)]),
     "acs_rank_sum_test": (C.c_int, [_P, _u32, _P, _u32, C.POINTER(_f64)]),
     "acs_gpu_distance_table": (C.c_int, [_desc, C.c_int, _P]),
     "acs_gpu_build_candidates": (C.c_int, [_desc, _u32, C.c_int, _P, C.POINTER(_u32)]),
@@ -93,6 +94,7 @@ SIGNATURES = {
     "acs_gpu_nccl_unique_id": (C.c_int, [_P]),
     "acs_gpu_island_init": (C.c_int, [_P, _P, C.c_int, C.c_int]),
     "acs_gpu_island_exchange": (C.c_int, [_P, C.POINTER(_i64)]),
+    "acs_gpu_island_exchange_local": (C.c_int, [_P, C.c_int, C.POINTER(_i64)]),
 }
 
 
@@ -137,6 +139,13 @@ def l2_read_bandwidth(device: int = 0, nbytes: int = 64 << 20) -> float:
     g = C.c_double(0.0)
     check(lib().acs_gpu_l2_read_bandwidth(device, nbytes, C.byref(g)), "l2_read_bandwidth")
     return g.value
+
+
+def l2_latency(device: int = 0, nbytes: int = 48 << 20):
+    """(L2 load-to-use ns, minimal selection step ns) -- acs_gpu_l2_latency."""
+    a, b = _f64(), _f64()
+    check(lib().acs_gpu_l2_latency(device, nbytes, C.byref(a), C.byref(b)), "l2_latency")
+    return a.value, b.value
 
 
 def device_count() -> int:

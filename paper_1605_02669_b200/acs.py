@@ -318,6 +318,16 @@ class Colony:
         N.check(self._lib.acs_gpu_island_exchange(self._h, C.byref(out)), "island_exchange")
         return out.value
 
+    @staticmethod
+    def island_exchange_local(colonies) -> int:
+        """Device-side exchange among colonies of this process on one GPU
+        (colonies[i] plays rank i); returns the global best length."""
+        arr = (C.c_void_p * len(colonies))(*[c._h.value for c in colonies])
+        out = C.c_int64()
+        N.check(N.lib().acs_gpu_island_exchange_local(arr, len(colonies), C.byref(out)),
+                "island_exchange_local")
+        return out.value
+
 
 @dataclass
 class RunReport:

@@ -16,6 +16,14 @@
 
 namespace acs_dev {
 
+// island exchange key (k_island_pack): L_gb << 16 | rank; at most 65536 ranks
+// and tour lengths below 2^47 (n < 2^24 cities at < 2^23 per edge)
+constexpr int kIslandRankBits = 16;
+constexpr int64_t kIslandRankMask = (int64_t{1} << kIslandRankBits) - 1;
+constexpr int kIslandMaxRanks = 1 << kIslandRankBits;
+constexpr int64_t kIslandMaxLen = (int64_t{1} << (63 - kIslandRankBits)) - 1;
+constexpr int64_t kNoIslandKey = INT64_MAX;
+
 // Selective memory, record-major: record u is one 128 B-aligned block
 // {vals[S] f64 | ids[S] u32 | tail u32} (S = 8: 100 B in one line), so reading
 // a record is one line instead of three, and two records never share a line
@@ -146,7 +154,12 @@ void launch_adopt_best(const uint32_t *tour, const int64_t *len, const DevInstan
                        const DevBest &B, cudaStream_t s);
 
 // island exchange helpers
+void launch_l2_chase(const uint32_t *next, uint32_t steps, uint32_t start, uint32_t *sink, cudaStream_t s);
+void launch_step_floor(const uint4 *rows, const double *tau, uint32_t nrows, uint32_t steps, uint32_t tour,
+                       uint32_t *sink, cudaStream_t s);
 void launch_island_pack(const int64_t *best_len, int rank, int64_t *key, cudaStream_t s);
+void launch_island_min(const int64_t *keys, int count, int64_t *out, cudaStream_t s);
+void launch_island_sum(const uint32_t *const *tours, int count, uint32_t n, uint32_t *out, cudaStream_t s);
 void launch_island_mask(const int64_t *key, int rank, const uint32_t *best_tour, uint32_t n,
                         uint32_t *x_tour, int64_t *x_len, cudaStream_t s);
 

@@ -224,6 +224,9 @@ struct acs_gpu_ctx {
     DBuf<int64_t> x_key;
     DBuf<uint32_t> x_tour;
     DBuf<int64_t> x_len;
+    DBuf<int64_t> xl_keys;            // in-process exchange (this ctx leads): one key per colony
+    DBuf<const uint32_t *> xl_tours;  // the colonies' masked tours
+    DBuf<uint32_t> xl_sum;            // their sum = the winner's tour
     nccl_comm comm = nullptr;
     int rank = 0, nranks = 1;
     // timing
@@ -390,6 +393,86 @@ int acs_gpu_l2_read_bandwidth(int device, uint64_t bytes, double *gbs) {
     cudaEventDestroy(e1);
     CUDA_TRY(cudaGetLastError());
     *gbs = static_cast<double>(count) * sizeof(uint4) * reps / (best * 1e-3) / 1e9;
+    return ACS_OK;
+}
+
+int acs_gpu_l2_latency(int device, uint64_t bytes, double *load_ns, double *step_ns) {
+    if (!load_ns || !step_ns || bytes < (4u << 20)) return fail(ACS_E_ARG, "null output or buffer below 4 MiB");
+    if (int rc = set_device(device)) return rc;
+    Stream st;
+    if (int rc = st.create()) return rc;
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    struct EvGuard {
+        cudaEvent_t a, b;
+        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
+    } eg{e0, e1};
+    auto timed = [&](auto &&launch) -> float {
+        float best = 1e30f;
+        for (int t = 0; t < 3; ++t) {
+            cudaEventRecord(e0, st.s);
+            launch();
+            cudaEventRecord(e1, st.s);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = std::min(best, ms);
+        }
+        return best;
+    };
+    DBuf<uint32_t> sink;
+    CUDA_TRY(sink.alloc(1));
+    uint64_t x = 0x2545F4914F6CDD1Dull;  // xorshift64 for the host-side layouts
+    auto rnd = [&x](uint64_t bound) {
+        x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+        return x % bound;
+    };
+    // (1) pointer chase: a random cycle (Sattolo) over the 128 B lines
+    {
+        const size_t lines = bytes / 128;
+        std::vector<uint32_t> perm(lines), h(lines * 32, 0u);
+        for (size_t i = 0; i < lines; ++i) perm[i] = static_cast<uint32_t>(i);
+        for (size_t i = lines - 1; i > 0; --i) std::swap(perm[i], perm[rnd(i)]);
+        for (size_t i = 0; i < lines; ++i) h[i * 32] = perm[i];
+        DBuf<uint32_t> buf;
+        CUDA_TRY(buf.alloc(h.size()));
+        CUDA_TRY(cudaMemcpyAsync(buf.p, h.data(), buf.bytes(), cudaMemcpyHostToDevice, st.s));
+        launch_l2_chase(buf.p, static_cast<uint32_t>(lines), 0, sink.p, st.s);  // warm: every line into L2
+        const uint32_t steps = 200000;
+        const float ms = timed([&] { launch_l2_chase(buf.p, steps, 1, sink.p, st.s); });
+        CUDA_TRY(cudaGetLastError());
+        *load_ns = static_cast<double>(ms) * 1e6 / steps;
+    }
+    // (2) minimal selection step over L2-resident rows (nrows x 512 B + 256 B)
+    {
+        const uint32_t nrows = static_cast<uint32_t>(std::min<uint64_t>(bytes / 768, 1u << 20));
+        std::vector<uint4> rows(static_cast<size_t>(nrows) * 32);
+        for (uint32_t r = 0; r < nrows; ++r)
+            for (int l = 0; l < 32; ++l) {
+                const uint32_t id = static_cast<uint32_t>((r + 1 + rnd(nrows - 1)) % nrows);
+                const double eta = 1.0 / static_cast<double>(1 + rnd(1000));
+                uint64_t b;
+                std::memcpy(&b, &eta, 8);
+                rows[static_cast<size_t>(r) * 32 + l] = make_uint4(id, 0u, static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32));
+            }
+        std::vector<double> tau(static_cast<size_t>(nrows) * 32, 1.0);
+        DBuf<uint4> drows;
+        DBuf<double> dtau;
+        CUDA_TRY(drows.alloc(rows.size()));
+        CUDA_TRY(dtau.alloc(tau.size()));
+        CUDA_TRY(cudaMemcpyAsync(drows.p, rows.data(), drows.bytes(), cudaMemcpyHostToDevice, st.s));
+        CUDA_TRY(cudaMemcpyAsync(dtau.p, tau.data(), dtau.bytes(), cudaMemcpyHostToDevice, st.s));
+        launch_l2_read(drows.p, drows.bytes() / sizeof(uint4), 2, sink.p, sms, st.s);  // warm into L2
+        launch_l2_read(reinterpret_cast<const uint4 *>(dtau.p), dtau.bytes() / sizeof(uint4), 2, sink.p, sms, st.s);
+        const uint32_t steps = 100000;
+        const float ms = timed([&] { launch_step_floor(drows.p, dtau.p, nrows, steps, 2048, sink.p, st.s); });
+        CUDA_TRY(cudaGetLastError());
+        *step_ns = static_cast<double>(ms) * 1e6 / steps;
+    }
+    CUDA_TRY(cudaStreamSynchronize(st.s));
     return ACS_OK;
 }
 
@@ -663,47 +746,58 @@ int acs_gpu_info(const acs_gpu_ctx *c, acs_ctx_info *info) {
     return ACS_OK;
 }
 
+// Iterations are issued in chunks of at most kIterChunk: the per-iteration
+// construct events and the device stats buffer are bounded by the chunk, not
+// by n_iter (a single call with a huge n_iter holds kIterChunk of each).
+constexpr uint32_t kIterChunk = 1024;
+
 int acs_gpu_iterate(acs_gpu_ctx *c, uint32_t n_iter, acs_iter_stats *out) {
     if (!c) return fail(ACS_E_ARG, "null ctx");
     if (n_iter == 0) return ACS_OK;
     CUDA_TRY(cudaSetDevice(c->device));
-    if (c->stats.count < n_iter) {
-        CUDA_TRY(c->stats.alloc(n_iter));
+    const uint32_t cap = std::min(n_iter, kIterChunk);
+    if (c->stats.count < cap) {
+        CUDA_TRY(c->stats.alloc(cap));
         c->best.stats = c->stats.p;
     }
-    if (int rc = c->ensure_events(2 + 2 * static_cast<size_t>(n_iter))) return rc;
+    if (int rc = c->ensure_events(2 + 2 * static_cast<size_t>(cap))) return rc;
     cudaStream_t s = c->stream.s;
     const DevInstance &I = c->inst.view;
     const int variant = static_cast<int>(c->params.variant);
     const int rng = static_cast<int>(c->params.rng);
-    CUDA_TRY(cudaEventRecord(c->events[0], s));
-    for (uint32_t i = 0; i < n_iter; ++i) {
-        CUDA_TRY(cudaEventRecord(c->events[2 + 2 * i], s));
-        if (variant == ACS_VARIANT_DEFERRED) {
-            if (launch_deferred(rng, I, c->colony, c->deferred, s) != 0)
-                return fail(ACS_E_CUDA, std::string("deferred: cooperative launch failed (colony not co-resident): ") +
-                                            cudaGetErrorString(cudaGetLastError()));
-        } else if (variant == ACS_VARIANT_SPM_SYNC) {
-            if (launch_spm_sync(rng, I, c->colony, c->spm_sync, s) != 0)
-                return fail(ACS_E_CUDA, std::string("spm-sync launch failed: ") + cudaGetErrorString(cudaGetLastError()));
-        } else {
-            launch_construct(variant, rng, I, c->colony, s);
-        }
-        CUDA_TRY(cudaEventRecord(c->events[3 + 2 * i], s));
-        launch_epilogue(!c->dense(), variant == ACS_VARIANT_ATOMIC, I, c->colony, c->best, i, s);
-        CUDA_TRY(cudaGetLastError());
-    }
-    CUDA_TRY(cudaEventRecord(c->events[1], s));
-    if (out)
-        CUDA_TRY(cudaMemcpyAsync(out, c->stats.p, sizeof(acs_iter_stats) * n_iter,
-                                 cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
     float total = 0, construct = 0;
-    CUDA_TRY(cudaEventElapsedTime(&total, c->events[0], c->events[1]));
-    for (uint32_t i = 0; i < n_iter; ++i) {
+    for (uint32_t done = 0; done < n_iter;) {
+        const uint32_t chunk = std::min(n_iter - done, kIterChunk);
+        CUDA_TRY(cudaEventRecord(c->events[0], s));
+        for (uint32_t i = 0; i < chunk; ++i) {
+            CUDA_TRY(cudaEventRecord(c->events[2 + 2 * i], s));
+            if (variant == ACS_VARIANT_DEFERRED) {
+                if (launch_deferred(rng, I, c->colony, c->deferred, s) != 0)
+                    return fail(ACS_E_CUDA, std::string("deferred: cooperative launch failed (colony not co-resident): ") +
+                                                cudaGetErrorString(cudaGetLastError()));
+            } else if (variant == ACS_VARIANT_SPM_SYNC) {
+                if (launch_spm_sync(rng, I, c->colony, c->spm_sync, s) != 0)
+                    return fail(ACS_E_CUDA, std::string("spm-sync launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+            } else {
+                launch_construct(variant, rng, I, c->colony, s);
+            }
+            CUDA_TRY(cudaEventRecord(c->events[3 + 2 * i], s));
+            launch_epilogue(!c->dense(), variant == ACS_VARIANT_ATOMIC, I, c->colony, c->best, i, s);
+            CUDA_TRY(cudaGetLastError());
+        }
+        CUDA_TRY(cudaEventRecord(c->events[1], s));
+        if (out)
+            CUDA_TRY(cudaMemcpyAsync(out + done, c->stats.p, sizeof(acs_iter_stats) * chunk,
+                                     cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
         float ms = 0;
-        CUDA_TRY(cudaEventElapsedTime(&ms, c->events[2 + 2 * i], c->events[3 + 2 * i]));
-        construct += ms;
+        CUDA_TRY(cudaEventElapsedTime(&ms, c->events[0], c->events[1]));
+        total += ms;
+        for (uint32_t i = 0; i < chunk; ++i) {
+            CUDA_TRY(cudaEventElapsedTime(&ms, c->events[2 + 2 * i], c->events[3 + 2 * i]));
+            construct += ms;
+        }
+        done += chunk;
     }
     c->last_total_ms = total;
     c->last_construct_ms = construct;
@@ -848,6 +942,7 @@ int acs_gpu_nccl_unique_id(void *uid) {
 
 int acs_gpu_island_init(acs_gpu_ctx *c, const void *uid, int nranks, int rank) {
     if (!c || !uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(ACS_E_ARG, "bad island init args");
+    if (nranks > kIslandMaxRanks) return fail(ACS_E_ARG, "island model supports at most 65536 ranks");
     if (int rc = g_nccl.load()) return rc;
     CUDA_TRY(cudaSetDevice(c->device));
     nccl_uid id;
@@ -864,6 +959,68 @@ int acs_gpu_island_init(acs_gpu_ctx *c, const void *uid, int nranks, int rank) {
     return ACS_OK;
 }
 
+int acs_gpu_island_exchange_local(acs_gpu_ctx *const *ctxs, int count, int64_t *global_best_len) {
+    if (!ctxs || count < 1) return fail(ACS_E_ARG, "island_exchange_local: no colonies");
+    if (count > kIslandMaxRanks) return fail(ACS_E_ARG, "island model supports at most 65536 ranks");
+    acs_gpu_ctx *lead = ctxs[0];
+    for (int i = 0; i < count; ++i) {
+        if (!ctxs[i]) return fail(ACS_E_ARG, "island_exchange_local: null ctx");
+        if (ctxs[i]->device != lead->device || ctxs[i]->n != lead->n)
+            return fail(ACS_E_ARG, "island_exchange_local: colonies must share the device and the instance size");
+        for (int j = 0; j < i; ++j)
+            if (ctxs[j] == ctxs[i]) return fail(ACS_E_ARG, "island_exchange_local: duplicate ctx");
+    }
+    CUDA_TRY(cudaSetDevice(lead->device));
+    cudaStream_t s = lead->stream.s;
+    const uint32_t n = lead->n;
+    for (int i = 0; i < count; ++i) {
+        acs_gpu_ctx *c = ctxs[i];
+        if (!c->x_tour.p) {
+            CUDA_TRY(c->x_tour.alloc(n));
+            CUDA_TRY(c->x_len.alloc(1));
+            CUDA_TRY(c->x_key.alloc(1));
+        }
+    }
+    if (lead->xl_keys.count < static_cast<size_t>(count)) {
+        CUDA_TRY(lead->xl_keys.alloc(count));
+        CUDA_TRY(lead->xl_tours.alloc(count));
+    }
+    if (!lead->xl_sum.p) CUDA_TRY(lead->xl_sum.alloc(n));
+    // order: every colony's pending iterations before the exchange, the
+    // exchange before any colony's next iteration
+    std::vector<cudaEvent_t> ev(count);
+    for (int i = 0; i < count; ++i) CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    struct EvGuard {
+        std::vector<cudaEvent_t> &e;
+        ~EvGuard() { for (cudaEvent_t x : e) cudaEventDestroy(x); }
+    } eg{ev};
+    for (int i = 1; i < count; ++i) {
+        CUDA_TRY(cudaEventRecord(ev[i], ctxs[i]->stream.s));
+        CUDA_TRY(cudaStreamWaitEvent(s, ev[i], 0));
+    }
+    std::vector<const uint32_t *> tours(count);
+    for (int i = 0; i < count; ++i) {
+        launch_island_pack(ctxs[i]->best_len.p, i, lead->xl_keys.p + i, s);
+        tours[i] = ctxs[i]->x_tour.p;
+    }
+    CUDA_TRY(cudaMemcpyAsync(lead->xl_tours.p, tours.data(), sizeof(const uint32_t *) * count,
+                             cudaMemcpyHostToDevice, s));
+    launch_island_min(lead->xl_keys.p, count, lead->x_key.p, s);               // = min-allreduce
+    for (int i = 0; i < count; ++i)
+        launch_island_mask(lead->x_key.p, i, ctxs[i]->best_tour.p, n, ctxs[i]->x_tour.p, ctxs[i]->x_len.p, s);
+    launch_island_sum(lead->xl_tours.p, count, n, lead->xl_sum.p, s);         // = sum-allreduce
+    for (int i = 0; i < count; ++i)
+        launch_adopt_best(lead->xl_sum.p, lead->x_len.p, ctxs[i]->inst.view, ctxs[i]->best, s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(ev[0], s));
+    for (int i = 1; i < count; ++i) CUDA_TRY(cudaStreamWaitEvent(ctxs[i]->stream.s, ev[0], 0));
+    if (global_best_len)
+        CUDA_TRY(cudaMemcpyAsync(global_best_len, lead->x_len.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    // the host pointer table is read by the copy above; events die with the guard
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return ACS_OK;
+}
+
 }  // extern "C"
 
 extern "C" int acs_gpu_island_exchange(acs_gpu_ctx *c, int64_t *global_best_len) {
@@ -871,7 +1028,7 @@ extern "C" int acs_gpu_island_exchange(acs_gpu_ctx *c, int64_t *global_best_len)
     if (!c->comm) return fail(ACS_E_NCCL, "island not initialised (acs_gpu_island_init)");
     CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t s = c->stream.s;
-    // 1. key = L_gb << 8 | rank; min over ranks -> best colony, ties to the lowest rank
+    // 1. key = L_gb << 16 | rank (kNoIslandKey before the first tour); min over ranks -> best colony, ties to the lowest rank
     launch_island_pack(c->best_len.p, c->rank, c->x_key.p, s);
     CUDA_TRY(cudaGetLastError());
     int r = g_nccl.all_reduce(c->x_key.p, c->x_key.p, 1, kNcclInt64, kNcclMin, c->comm, s);

@@ -1492,16 +1492,52 @@ __global__ void k_adopt_best(const uint32_t *tour, const int64_t *len, uint32_t 
     if (threadIdx.x == 0) *B.len = *len;
 }
 
+// Island key: L_gb << kIslandRankBits | rank, so a min-allreduce picks the best
+// colony with ties to the lowest rank.  A colony with no tour yet (L_gb still
+// the LLONG_MAX sentinel) -- or a length too large to shift -- packs the
+// sentinel kNoIslandKey itself: it never wins against a real tour, and if
+// every rank holds it the exchange adopts nothing.
 __global__ void k_island_pack(const int64_t *best_len, int rank, int64_t *key) {
-    *key = (*best_len << 8) | rank;
+    const int64_t l = *best_len;
+    *key = (l < 0 || l > kIslandMaxLen) ? kNoIslandKey : ((l << kIslandRankBits) | rank);
 }
 
 __global__ void k_island_mask(const int64_t *key, int rank, const uint32_t *tour, uint32_t n,
                               uint32_t *x_tour, int64_t *x_len) {
-    const bool mine = static_cast<int>(*key & 0xFF) == rank;
+    const int64_t k = *key;
+    const bool none = k == kNoIslandKey;
+    const bool mine = !none && static_cast<int>(k & kIslandRankMask) == rank;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         x_tour[i] = mine ? tour[i] : 0u;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *x_len = *key >> 8;
+    // LLONG_MAX: k_adopt_best's strict < never takes it
+    if (blockIdx.x == 0 && threadIdx.x == 0) *x_len = none ? LLONG_MAX : (k >> kIslandRankBits);
+}
+
+// In-process exchange (acs_gpu_island_exchange_local): the two NCCL
+// all-reduces of the multi-GPU path, restated as device reductions over the
+// colonies of one process on one GPU -- min over the packed keys, and the sum
+// of the masked tours (only the winner's is non-zero).  The pack / mask /
+// adopt kernels around them are the ones the NCCL path runs.
+__global__ void k_island_min(const int64_t *keys, int count, int64_t *out) {
+    int64_t k = kNoIslandKey;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) k = min(k, keys[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) k = min(k, static_cast<int64_t>(shfl_xor_u64(static_cast<uint64_t>(k), o)));
+    __shared__ int64_t part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = k;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) k = min(k, part[w]);
+        *out = k;
+    }
+}
+
+__global__ void k_island_sum(const uint32_t *const *tours, int count, uint32_t n, uint32_t *out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t x = 0;
+        for (int r = 0; r < count; ++r) x += tours[r][i];
+        out[i] = x;
+    }
 }
 
 // ============================================================ launchers
@@ -1667,6 +1703,14 @@ void launch_island_mask(const int64_t *key, int rank, const uint32_t *best_tour,
                         uint32_t *x_tour, int64_t *x_len, cudaStream_t s) {
     k_island_mask<<<std::min<unsigned>(blocks_for(n, 256), 64), 256, 0, s>>>(key, rank, best_tour, n,
                                                                             x_tour, x_len);
+}
+
+void launch_island_min(const int64_t *keys, int count, int64_t *out, cudaStream_t s) {
+    k_island_min<<<1, 256, 0, s>>>(keys, count, out);
+}
+
+void launch_island_sum(const uint32_t *const *tours, int count, uint32_t n, uint32_t *out, cudaStream_t s) {
+    k_island_sum<<<std::min<unsigned>(blocks_for(n, 256), 64), 256, 0, s>>>(tours, count, n, out);
 }
 
 }  // namespace acs_dev

@@ -2,7 +2,7 @@
 every X iterations.
 
 The device path is ``Colony.island_init`` / ``Colony.island_exchange``: NCCL
-inside libacs_b200.so (min-allreduce of ``L_gb << 8 | rank``, then a
+inside libacs_b200.so (min-allreduce of ``L_gb << 16 | rank``, then a
 sum-allreduce in which only the winner contributes its tour, then a device-
 side strictly-better adoption) -- no host round trip.
 
@@ -16,11 +16,28 @@ from __future__ import annotations
 import numpy as np
 
 
+RANK_BITS = 16
+NO_KEY = (1 << 63) - 1          # no tour yet: never wins, adopts nothing
+MAX_LEN = (1 << (63 - RANK_BITS)) - 1
+
+
 def exchange_key(best_len: int, rank: int) -> int:
-    """min over ranks selects the best colony; ties go to the lowest rank."""
-    if rank < 0 or rank > 0xFF:
-        raise ValueError("island rank must fit in 8 bits")
-    return (int(best_len) << 8) | rank
+    """min over ranks selects the best colony; ties go to the lowest rank.
+    Same layout as the device path (k_island_pack): L_gb << 16 | rank, and
+    the sentinel NO_KEY for a colony that has no tour yet."""
+    if rank < 0 or rank >= (1 << RANK_BITS):
+        raise ValueError("island rank must fit in 16 bits")
+    best_len = int(best_len)
+    if best_len < 0 or best_len > MAX_LEN:
+        return NO_KEY
+    return (best_len << RANK_BITS) | rank
+
+
+def decode_key(key: int):
+    """(winner rank, global best length); (None, None) for NO_KEY."""
+    if key == NO_KEY:
+        return None, None
+    return key & ((1 << RANK_BITS) - 1), key >> RANK_BITS
 
 
 def exchange_host(colony, dist, group=None) -> int:
@@ -33,8 +50,9 @@ def exchange_host(colony, dist, group=None) -> int:
     order, length = colony.best()
     key = torch.tensor([exchange_key(length, rank)], dtype=torch.int64)
     dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
-    k = int(key.item())
-    winner, glen = k & 0xFF, k >> 8
+    winner, glen = decode_key(int(key.item()))
+    if winner is None:  # no rank has a tour yet
+        return length
     buf = torch.from_numpy(np.ascontiguousarray(order, np.int64)) if rank == winner \
         else torch.zeros(len(order), dtype=torch.int64)
     dist.broadcast(buf, src=dist.get_global_rank(group, winner) if group is not None else winner, group=group)

@@ -18,6 +18,11 @@ def test_reference_arm_json():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["metric"].startswith("constructed tours/sec at pr2392")
+    # the same workload as the GPU arm: one persistent colony of m = n ants
+    c = d["config"]
+    assert c["instance"] == "d198" and c["ants_per_gpu"] == 198 and c["rng"] == "philox"
+    assert c["reference_mode"] == {"mode": "relaxed", "memory": "dense", "consistent": 1}
+    assert "persistent 198-ant colony" in d["cpu_baseline"]["sample"]
 
 
 def test_reference_arm_other_ranks_exit_quietly():

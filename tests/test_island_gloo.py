@@ -10,7 +10,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1605_02669_b200.island import exchange_host, exchange_key
+from paper_1605_02669_b200.island import NO_KEY, decode_key, exchange_host, exchange_key
 
 
 class FakeColony:
@@ -75,5 +75,40 @@ def test_exchange_two_ranks(lens):
 def test_exchange_key_order():
     assert exchange_key(5, 3) < exchange_key(6, 0)
     assert exchange_key(5, 0) < exchange_key(5, 1)
+    assert exchange_key(5, 300) < exchange_key(6, 0)  # 16-bit ranks (> 256 ranks)
+    assert decode_key(exchange_key(12345, 4000)) == (4000, 12345)
     with pytest.raises(ValueError):
-        exchange_key(5, 256)
+        exchange_key(5, 1 << 16)
+    # a colony without a tour (LLONG_MAX sentinel) never wins and adopts nothing
+    assert exchange_key((1 << 63) - 1, 0) == NO_KEY
+    assert exchange_key(10**9, 7) < NO_KEY
+    assert decode_key(NO_KEY) == (None, None)
+
+
+def _worker_empty(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank 1 has not iterated yet (sentinel length); rank 0 has a tour
+    length = 700 if rank == 0 else (1 << 63) - 1
+    col = FakeColony(np.arange(10)[::-1] if rank == 0 else np.zeros(10), length)
+    g = exchange_host(col, dist)
+    q.put((rank, g, col.length, col.best()[0].tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_exchange_before_first_iteration():
+    """a rank still holding the LLONG_MAX sentinel must not win."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_empty, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, g, length, order in res:
+        assert g == 700 and length == 700 and order == list(range(10))[::-1]
