@@ -203,6 +203,27 @@ __device__ __forceinline__ int warp_argmax_pos(double score, bool valid) {
     return __ffs(win) - 1;
 }
 
+// The same argmax (non-negative doubles, ties -> lowest lane) as three
+// dependent REDUX ops and no VOTE / FLO / SHFL on the chain (measured on
+// B200: REDUX 18 cycles, VOTE 23, BREV+FLO 36, SHFL 32): max of the high
+// words, max of the low words among those lanes, then one max over the key
+// (31 - lane) << 24 | id, which yields the lowest winning lane and its node
+// id together.  `id` < 2^24.  Returns false when no lane is valid.
+__device__ __forceinline__ bool warp_argmax_id(double score, bool valid, uint32_t id, int lane, int &pos,
+                                               uint32_t &v) {
+    const uint64_t b = dbits(score);
+    const uint32_t hk = valid ? static_cast<uint32_t>(b >> 32) + 1u : 0u;  // finite: hi + 1 never wraps
+    const uint32_t mh = __reduce_max_sync(kFull, hk);
+    const bool t1 = valid && hk == mh;
+    const uint32_t lo = static_cast<uint32_t>(b);
+    const uint32_t ml = __reduce_max_sync(kFull, t1 ? lo : 0u);
+    const bool t2 = t1 && lo == ml;
+    const uint32_t key = __reduce_max_sync(kFull, t2 ? ((31u - static_cast<uint32_t>(lane)) << 24) | id : 0u);
+    pos = 31 - static_cast<int>(key >> 24);
+    v = key & 0x00FFFFFFu;
+    return mh != 0u;
+}
+
 // Roulette (Eq.2, D8, P5): sequential prefix in candidate
 // order computed by lane 0 in shared scratch, then one ballot.  Zero weights
 // stand for filtered-out (visited) slots: x + 0.0 == x keeps it bit-exact.

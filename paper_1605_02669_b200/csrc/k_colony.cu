@@ -342,16 +342,18 @@ __device__ __forceinline__ void select_step(const DevInstance &I, const DevColon
         const double score = unv ? __dmul_rn(tau_lane, eb) : 0.0;
         int pos;
         if (la.greedy(C)) {
-            pos = warp_argmax_pos(score, unv);
+            uint32_t v;
+            warp_argmax_id(score, unv, c, lane, pos, v);  // um != 0: a lane is valid
+            o.v = v;
             o.kind = 0;
         } else {
             rng.advance();  // commit q
             const double r = uniform01(rng);
             pos = warp_roulette_pos(score, um, r, scratch, lane);
+            o.v = __shfl_sync(kFull, c, pos);
             o.kind = 1;
         }
         o.pos = pos;
-        o.v = __shfl_sync(kFull, c, pos);
         o.mirror = __shfl_sync(kFull, el.x >> 24, pos);
         o.d = static_cast<int32_t>(__shfl_sync(kFull, el.y, pos));
         o.tau_old = __shfl_sync(kFull, tau_lane, pos);
@@ -533,6 +535,14 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
         uint32_t mprev = kEmpty;
 
         for (uint32_t t = 1; t < n; ++t) {
+            // The copy of the previous edge in THIS row (cur -> prev) is written
+            // by the lane holding prev, after the row's own load has completed.
+            // Its operands depend on the row only, so they are formed here, off
+            // the selection chain, and the store is issued after the next
+            // row's loads.
+            const bool mw = (kLean || static_cast<uint32_t>(lane) < C.L) && (el.x & kIdMask) == mprev;
+            const size_t mi = static_cast<size_t>(cur) * 32 + lane;
+            const double mval = kAtomic ? 0.0 : affine(tl, C.c_l, C.c_0);
             Step st;
             if constexpr (kAtomic) {
                 const double tv = trail_value(tl, cl, C, pw_lo, pw_hi);
@@ -551,14 +561,6 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
                             },
                             st);
             }
-            if (st.kind) wc.count(st.kind, n - t);  // greedy steps are derived at flush
-            // the copy of the previous edge in THIS row (v -> prev) is written now,
-            // by the lane holding prev, after the row's own load has completed
-            if ((kLean || static_cast<uint32_t>(lane) < C.L) && (el.x & kIdMask) == mprev) {
-                if constexpr (kAtomic) red_add1(C.cntc + static_cast<size_t>(cur) * 32 + lane);
-                else st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
-            }
-            mprev = kEmpty;
             // Next dependent row load, issued as soon as v is known: the writes
             // below touch rows u (tauc, tau) and v of the DENSE matrix only --
             // the one copy in tauc row v is written a step late (above), because
@@ -568,6 +570,12 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
             el = __ldg(C.rows + ri);
             tl = ld_relaxed(C.tauc + ri);
             if constexpr (kAtomic) cl = ld_relaxed_u32(C.cntc + ri);
+            if (mw) {
+                if constexpr (kAtomic) red_add1(C.cntc + mi);
+                else st_relaxed(C.tauc + mi, mval);
+            }
+            mprev = kEmpty;
+            if (st.kind) wc.count(st.kind, n - t);  // greedy steps are derived at flush
             if (kLean || ++kc == C.k) {  // D9 per-ant edge counter (warp-uniform)
                 kc = 0;
                 if constexpr (!kLean) ++wc.updates;
@@ -620,6 +628,221 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
                     const double told = ld_relaxed(C.tau + static_cast<size_t>(cur) * n + start);
                     st_relaxed((dense ? C.tau : C.tauc) + k, affine(told, C.c_l, C.c_0));
                 }
+            }
+        }
+        if (lane == 0) C.lens[a] = len + dclose;
+        wc.flush(C.counters, lane, n - 1);
+        __syncwarp();
+    }
+}
+
+// ============================================================ lean whole tour
+
+// Predicated single-instruction stores (no branch, no BSSY/BSYNC around them).
+__device__ __forceinline__ void st_relaxed_if(bool p, double *ptr, double v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.relaxed.gpu.global.b64 [%1], %2; }" ::"r"(
+                     static_cast<int>(p)),
+                 "l"(ptr), "l"(dbits(v))
+                 : "memory");
+}
+__device__ __forceinline__ void red_add_if(bool p, uint32_t *ptr, uint32_t one) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q red.relaxed.gpu.global.add.u32 [%1], %2; }" ::"r"(
+                     static_cast<int>(p)),
+                 "l"(ptr), "r"(one)
+                 : "memory");
+}
+__device__ __forceinline__ void st_u32_if(bool p, uint32_t *ptr, uint32_t v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.global.u32 [%1], %2; }" ::"r"(static_cast<int>(p)),
+                 "l"(ptr), "r"(v)
+                 : "memory");
+}
+
+// ATOMIC trail value f^c(b) (trail_value) for the lean kernel: c_l^c from the
+// static shared tables, every operand formed unconditionally and the three
+// cases (c = 0, 1, >= 2) picked by selects -- no branch on the chain.
+constexpr uint32_t kLeanPwHi = 64;  // c < 512 * 64 pending updates (m <= 31744)
+__device__ __forceinline__ double trail_value_sel(double b, uint32_t c, const DevColony &C, const double *pw) {
+    const double p = __dmul_rn(pw[c & 511u], pw[512u + min(c >> 9, kLeanPwHi - 1)]);
+    const double one = affine(b, C.c_l, C.c_0);
+    const double closed = __dadd_rn(C.tau_min, __dmul_rn(p, __dsub_rn(b, C.tau_min)));
+    const double x = c >= 2u ? closed : one;
+    return c == 0u ? b : x;
+}
+__device__ __forceinline__ void sts_if(bool p, uint32_t *ptr, uint32_t v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.shared.u32 [%1], %2; }" ::"r"(static_cast<int>(p)),
+                 "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ptr))), "r"(v)
+                 : "memory");
+}
+
+// K4 for the paper's configuration (k = 1, 32-slot candidate lists), dense
+// memory: ATOMIC (kMode 1) / RELAXED (kMode 0).  Same semantics and RNG
+// protocol as k_construct_dense; the step is laid out for the shortest
+// dependent chain and the fewest warp instructions:
+//   * chain: row load -> visited word (LDS) -> score -> warp_argmax_id (three
+//     REDUX, winner id included) -> next row address -> next loads;
+//   * a greedy step needs no ballot (argmax validity = non-empty filtered set)
+//     and no select of the masked score;
+//   * everything else -- pheromone update stores, the late mirror copy, the
+//     visited mark, RNG commit, route, length, counters -- is issued after the
+//     next row's loads, as predicated stores without branches;
+//   * the visited mark of a candidate step is the store of the word the
+//     winning lane already loaded for its test (no second LDS).
+template <int kMode, class RNG, int kRegs>
+__global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
+    constexpr bool kAtomic = kMode == 1;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double s_pw[kAtomic ? 512 + kLeanPwHi : 1];  // ATOMIC: c_l^j | c_l^(512k)
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
+    uint32_t *vis = reinterpret_cast<uint32_t *>(smem + wpb * 32 * sizeof(double)) + static_cast<size_t>(wib) * I.words;
+    if constexpr (kAtomic) {
+        for (uint32_t i = threadIdx.x; i < 512 + kLeanPwHi; i += blockDim.x)
+            s_pw[i] = i < 512 + C.pw_hi_n ? C.pw_lo[i] : 0.0;
+        __syncthreads();
+    }
+    const uint64_t it = *C.iter;
+    const uint32_t n = I.n;
+    const uint32_t one = 1u;
+    WarpCounters wc;
+
+    for (uint32_t a = blockIdx.x * wpb + wib; a < C.m; a += gridDim.x * wpb) {
+        for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
+        RNG rng;
+        rng_init(rng, C, it, a);
+        const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));  // P1.1
+        size_t ri = static_cast<size_t>(start) * 32 + lane;
+        uint4 el = __ldg(C.rows + ri);
+        double tl = ld_relaxed(C.tauc + ri);
+        uint32_t cl = kAtomic ? ld_relaxed_u32(C.cntc + ri) : 0u;
+        __syncwarp();
+        if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
+        __syncwarp();
+        uint32_t *route = C.routes + static_cast<size_t>(a) * n;
+        uint32_t rbuf = start, cur = start;
+        long long len = 0;
+        Lookahead<RNG> la;
+        la.prepare(rng);
+        uint32_t mprev = kEmpty;  // row cur owes the late copy of edge (prev, cur)
+
+        for (uint32_t t = 1; t < n; ++t) {
+            const uint32_t c = el.x & kIdMask;
+            uint32_t *vw = vis + (c >> 5);
+            const uint32_t word = *vw, bit = 1u << (c & 31);
+            const bool unv = !(word & bit);
+            const double tv = kAtomic ? trail_value_sel(tl, cl, C, s_pw) : tl;
+            const double score = __dmul_rn(tv, __hiloint2double(static_cast<int>(el.w), static_cast<int>(el.z)));
+            // off-chain operands of this row's late mirror copy
+            const bool mw = c == mprev;
+            const size_t mi = static_cast<size_t>(cur) * 32 + lane;
+            const double mval = kAtomic ? 0.0 : affine(tl, C.c_l, C.c_0);
+            int pos;
+            uint32_t v;
+            int kind;
+            double tau_old;
+            int32_t d;
+            bool cand;
+            if (la.greedy(C)) {
+                cand = warp_argmax_id(score, unv, c, lane, pos, v);
+                kind = 0;
+            } else {
+                const unsigned um = __ballot_sync(kFull, unv);
+                cand = um != 0u;
+                if (cand) {
+                    rng.advance();  // commit q (P1: only when the filtered set is non-empty)
+                    const double r = uniform01(rng);
+                    pos = warp_roulette_pos(unv ? score : 0.0, um, r, scratch, lane);
+                    v = __shfl_sync(kFull, c, pos);
+                }
+                kind = 1;
+            }
+            if (cand) {
+                tau_old = __shfl_sync(kFull, tv, pos);
+                d = static_cast<int32_t>(__shfl_sync(kFull, el.y, pos));
+            } else {  // every candidate visited: fallback (no draw, P1)
+                Step st;
+                if constexpr (kAtomic) {
+                    fallback_scan(I, C, vis, cur,
+                                  [&](uint32_t x, bool act) {
+                                      if (!act) return 0.0;
+                                      const size_t k = static_cast<size_t>(cur) * n + x;
+                                      return trail_value_sel(ld_relaxed(C.tau + k), ld_relaxed_u32(C.cnt + k), C, s_pw);
+                                  },
+                                  lane, st);
+                } else {
+                    fallback_scan(I, C, vis, cur,
+                                  [&](uint32_t x, bool act) {
+                                      return act ? ld_relaxed(C.tau + static_cast<size_t>(cur) * n + x) : 0.0;
+                                  },
+                                  lane, st);
+                }
+                v = st.v;
+                pos = -1;
+                tau_old = st.tau_old;
+                d = st.d;
+                kind = 2;
+                if (lane == 0) vis[v >> 5] |= 1u << (v & 31);  // (a candidate step's mark: below)
+            }
+            // ---- next row: issued as soon as v is known
+            ri = static_cast<size_t>(v) * 32 + lane;
+            el = __ldg(C.rows + ri);
+            tl = ld_relaxed(C.tauc + ri);
+            if constexpr (kAtomic) cl = ld_relaxed_u32(C.cntc + ri);
+            // ---- off the chain
+            // late copy of the previous edge in row cur (its load has completed)
+            if constexpr (kAtomic) red_add_if(mw, C.cntc + mi, one);
+            else st_relaxed_if(mw, C.tauc + mi, mval);
+            // this edge: lane 0 tau[u][v], lane 1 tau[v][u], lane 2 tauc[u][pos]
+            // (lane 3's tauc[v][mirror] is next step's late copy)
+            {
+                const bool l1 = lane == 1;
+                const size_t di = static_cast<size_t>(l1 ? v : cur) * n + (l1 ? cur : v);
+                const size_t ci = static_cast<size_t>(cur) * 32 + static_cast<uint32_t>(pos);
+                const bool wr = lane < 2 || (lane == 2 && pos >= 0);
+                if constexpr (kAtomic) red_add_if(wr, lane < 2 ? C.cnt + di : C.cntc + ci, one);
+                else st_relaxed_if(wr, lane < 2 ? C.tau + di : C.tauc + ci, affine(tau_old, C.c_l, C.c_0));
+            }
+            mprev = cur;
+            // visited mark: the winning lane stores the word it tested (pos = -1
+            // after a fallback, which marked v itself)
+            sts_if(lane == pos, vw, word | bit);
+            // RNG: commit a greedy step's q draw, peek the next one
+            if (kind == 0) rng.advance();
+            la.prepare(rng);
+            wc.roulette += kind == 1;
+            wc.fallback += kind == 2;
+            wc.fb_elems += kind == 2 ? n - t : 0u;
+            len += d;
+            route_put(route, rbuf, t, v, lane);
+            cur = v;
+            __syncwarp();
+        }
+        route_flush(route, rbuf, n - 1, lane);
+        wc.updates += n - 1;
+        // last step's late mirror copy (el/tl hold row `cur`)
+        if ((el.x & kIdMask) == mprev) {
+            if constexpr (kAtomic) red_add1(C.cntc + static_cast<size_t>(cur) * 32 + lane);
+            else st_relaxed(C.tauc + static_cast<size_t>(cur) * 32 + lane, affine(tl, C.c_l, C.c_0));
+        }
+        __syncwarp();
+        // closing edge (cur -> start) is edge n of the ant (D9, k = 1: due)
+        int pos;
+        uint32_t mirror;
+        int32_t dclose;
+        bool have_d;
+        closing_slots(C, cur, start, lane, pos, mirror, dclose, have_d);
+        if (!have_d)
+            dclose = tsplib_distance(I.type, __ldg(I.xs + cur), __ldg(I.ys + cur), __ldg(I.xs + start),
+                                     __ldg(I.ys + start));
+        ++wc.updates;
+        bool dense;
+        size_t k;
+        if (copy_index(n, cur, start, pos, mirror, lane, dense, k)) {
+            if constexpr (kAtomic) {
+                red_add1((dense ? C.cnt : C.cntc) + k);
+            } else {
+                const double told = ld_relaxed(C.tau + static_cast<size_t>(cur) * n + start);
+                st_relaxed((dense ? C.tau : C.tauc) + k, affine(told, C.c_l, C.c_0));
             }
         }
         if (lane == 0) C.lens[a] = len + dclose;
@@ -1573,9 +1796,18 @@ static void launch_tour_kernel(K kernel, const DevInstance &I, const DevColony &
 // waves instead of four (measured: relaxed 41.9 -> 38.2, atomic 57.9 -> 49.8 ms).
 constexpr int kWideRegs = 72;
 
+template <int kMode, class RNG, int kRegs, bool kLean>
+constexpr auto dense_kernel() {
+#ifndef ACS_X_OLD_LEAN
+    if constexpr (kLean) return k_tour_lean<kMode, RNG, kRegs>;
+    else
+#endif
+        return k_construct_dense<kMode, RNG, kRegs, kLean>;
+}
+
 template <int kMode, class RNG, bool kLean>
 static void launch_dense_t(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw) {
-    auto narrow = k_construct_dense<kMode, RNG, kMaxRegs, kLean>;
+    auto narrow = dense_kernel<kMode, RNG, kMaxRegs, kLean>();
     if (!one_warp) {
         // The narrow-vs-wide decision (occupancy query) is made once per
         // (device, shared memory, m) and remembered per host thread: it costs
@@ -1595,7 +1827,7 @@ static void launch_dense_t(const DevInstance &I, const DevColony &C, bool one_wa
             memo = Memo{dev, smem, C.m, static_cast<uint64_t>(per_sm) * sms * (kBlock / 32) < C.m};
         }
         if (memo.wide) {
-            launch_tour_kernel(k_construct_dense<kMode, RNG, kWideRegs, kLean>, I, C, false, s, pw);
+            launch_tour_kernel(dense_kernel<kMode, RNG, kWideRegs, kLean>(), I, C, false, s, pw);
             return;
         }
     }
@@ -1604,8 +1836,12 @@ static void launch_dense_t(const DevInstance &I, const DevColony &C, bool one_wa
 
 template <int kMode, class RNG>
 static void launch_dense(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw = false) {
-    if (C.k == 1 && C.L == 32 && !one_warp) {
+    if (C.k == 1 && C.L == 32 && !one_warp && (!pw || C.pw_hi_n <= kLeanPwHi)) {
+#ifdef ACS_X_OLD_LEAN
         launch_dense_t<kMode, RNG, true>(I, C, one_warp, s, pw);
+#else
+        launch_dense_t<kMode, RNG, true>(I, C, one_warp, s, false);  // k_tour_lean: static power tables
+#endif
         return;
     }
     launch_dense_t<kMode, RNG, false>(I, C, one_warp, s, pw);

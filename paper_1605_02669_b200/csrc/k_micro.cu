@@ -11,7 +11,7 @@
 //                 row load {id, eta^beta} + one 256 B trail load (the two
 //                 loads every construction step issues), the shared-memory
 //                 visited test, the score multiply, the exact warp argmax
-//                 (warp_argmax_pos), the winner's id by shuffle, the visited
+//                 with the winner's id (warp_argmax_id: three REDUX), the visited
 //                 update -- and the next row is the winner's.  No RNG, no
 //                 bookkeeping, no pheromone update: what no implementation of
 //                 a warp-per-ant step over L2-resident rows can undercut.
@@ -46,8 +46,9 @@ __global__ void k_step_floor(const uint4 *__restrict__ rows, const double *tau, 
         const uint32_t c = el.x;
         const bool unv = !visited(vis, c);
         const double score = unv ? __dmul_rn(t, __hiloint2double(static_cast<int>(el.w), static_cast<int>(el.z))) : 0.0;
-        const int pos = warp_argmax_pos(score, unv);
-        const uint32_t v = __shfl_sync(kFull, c, pos < 0 ? 0 : pos);
+        int pos;
+        uint32_t v;
+        if (!warp_argmax_id(score, unv, c, lane, pos, v)) v = (cur + 1) % nrows;  // all visited (rare)
         vis[v >> 5] |= 1u << (v & 31);
         cur = v;
         __syncwarp();

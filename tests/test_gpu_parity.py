@@ -179,6 +179,41 @@ def test_atomic_single_ant_equals_seq(acs, orc, gpu):
     assert np.array_equal(tau.view(np.uint64), o["tau"].view(np.uint64))
 
 
+@pytest.mark.parametrize("variant", ["atomic", "relaxed"])
+@pytest.mark.parametrize("rng", ["xoshiro", "philox"])
+@pytest.mark.parametrize("q0", [-1.0, 0.0, 0.7])
+def test_lean_kernel_single_ant_equals_seq(acs, orc, gpu, variant, rng, q0):
+    """k = 1 with 32-slot lists runs the lean tour kernel (k_tour_lean): with
+    one ant it must reproduce SEQ bit for bit -- routes, trace, pheromone,
+    step counters -- for both RNG engines, greedy, roulette and mixed steps."""
+    I = O.load("d198")
+    p = acs.AcsParams(variant=variant, m=1, seed=12, rng=rng, q0=q0)
+    with acs.Colony(to_acs(acs, I), p) as col:
+        st = col.iterate(6)
+        tau = col.pheromone()
+        routes, lens = col.routes()
+        cnt = col.counters()
+    o = orc.run(I, m=1, iterations=6, seed=12, mode=O.SEQ, want_tau=True, q0=q0,
+                rng=O.PHILOX if rng == "philox" else O.XOSHIRO)
+    assert st["global_best_len"].tolist() == o["trace"].tolist()
+    assert (routes == o["routes"]).all() and lens.tolist() == o["lengths"].tolist()
+    assert np.array_equal(tau.view(np.uint64), o["tau"].view(np.uint64))
+    for k in ("fallback_steps", "greedy_steps", "roulette_steps", "local_updates"):
+        assert cnt[k] == o[k], k
+
+
+def test_lean_kernel_single_ant_pr2392(acs, orc, gpu):
+    """The headline instance through the lean kernel, one ant: bit-exact SEQ."""
+    I = O.load("pr2392")
+    p = acs.AcsParams(variant="relaxed", m=1, seed=3, rng="philox")
+    with acs.Colony(to_acs(acs, I), p) as col:
+        st = col.iterate(2)
+        tau = col.pheromone()
+    o = orc.run(I, m=1, iterations=2, seed=3, mode=O.SEQ, want_tau=True, rng=O.PHILOX)
+    assert st["global_best_len"].tolist() == o["trace"].tolist()
+    assert np.array_equal(tau.view(np.uint64), o["tau"].view(np.uint64))
+
+
 def test_sync_more_ants_than_resident_warps(acs, orc, gpu):
     """m > resident warps: the cooperative deferred kernel runs several ants
     per warp (state in shared memory) and must stay bit-exact."""
