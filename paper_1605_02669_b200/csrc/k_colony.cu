@@ -720,7 +720,7 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
         __syncwarp();
         uint32_t *route = C.routes + static_cast<size_t>(a) * n;
         uint32_t rbuf = start, cur = start;
-        long long len = 0;
+        long long lenl = 0;  // this lane's share of the tour length (edges chosen from its slot)
         Lookahead<RNG> la;
         la.prepare(rng);
         uint32_t mprev = kEmpty;  // row cur owes the late copy of edge (prev, cur)
@@ -732,19 +732,18 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             const bool unv = !(word & bit);
             const double tv = kAtomic ? trail_value_sel(tl, cl, C, s_pw) : tl;
             const double score = __dmul_rn(tv, __hiloint2double(static_cast<int>(el.w), static_cast<int>(el.z)));
-            // off-chain operands of this row's late mirror copy
+            // off-chain: this lane's copy tauc[cur][lane] gets f(its trail) if it
+            // holds the chosen slot or the late mirror copy (the slot of prev)
             const bool mw = c == mprev;
             const size_t mi = static_cast<size_t>(cur) * 32 + lane;
             const double mval = kAtomic ? 0.0 : affine(tl, C.c_l, C.c_0);
+            const int32_t dl = static_cast<int32_t>(el.y);
             int pos;
             uint32_t v;
-            int kind;
-            double tau_old;
-            int32_t d;
             bool cand;
-            if (la.greedy(C)) {
+            const bool greedy = la.greedy(C);
+            if (greedy) {
                 cand = warp_argmax_id(score, unv, c, lane, pos, v);
-                kind = 0;
             } else {
                 const unsigned um = __ballot_sync(kFull, unv);
                 cand = um != 0u;
@@ -753,13 +752,10 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
                     const double r = uniform01(rng);
                     pos = warp_roulette_pos(unv ? score : 0.0, um, r, scratch, lane);
                     v = __shfl_sync(kFull, c, pos);
+                    ++wc.roulette;
                 }
-                kind = 1;
             }
-            if (cand) {
-                tau_old = __shfl_sync(kFull, tv, pos);
-                d = static_cast<int32_t>(__shfl_sync(kFull, el.y, pos));
-            } else {  // every candidate visited: fallback (no draw, P1)
+            if (!cand) {  // every candidate visited: fallback (no draw, P1)
                 Step st;
                 if constexpr (kAtomic) {
                     fallback_scan(I, C, vis, cur,
@@ -778,47 +774,57 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
                 }
                 v = st.v;
                 pos = -1;
-                tau_old = st.tau_old;
-                d = st.d;
-                kind = 2;
-                if (lane == 0) vis[v >> 5] |= 1u << (v & 31);  // (a candidate step's mark: below)
+                // the non-candidate edge's dense copies: lane 0 tau[u][v], lane 1 tau[v][u]
+                if (lane < 2) {
+                    const size_t di = lane ? static_cast<size_t>(v) * n + cur : static_cast<size_t>(cur) * n + v;
+                    if constexpr (kAtomic) red_add1(C.cnt + di);
+                    else st_relaxed(C.tau + di, affine(st.tau_old, C.c_l, C.c_0));
+                }
+                if (lane == 0) {
+                    vis[v >> 5] |= 1u << (v & 31);
+                    lenl += st.d;
+                }
+                ++wc.fallback;
+                wc.fb_elems += n - t;
             }
             // ---- next row: issued as soon as v is known
             ri = static_cast<size_t>(v) * 32 + lane;
             el = __ldg(C.rows + ri);
             tl = ld_relaxed(C.tauc + ri);
             if constexpr (kAtomic) cl = ld_relaxed_u32(C.cntc + ri);
-            // ---- off the chain
-            // late copy of the previous edge in row cur (its load has completed)
-            if constexpr (kAtomic) red_add_if(mw, C.cntc + mi, one);
-            else st_relaxed_if(mw, C.tauc + mi, mval);
-            // this edge: lane 0 tau[u][v], lane 1 tau[v][u], lane 2 tauc[u][pos]
-            // (lane 3's tauc[v][mirror] is next step's late copy)
-            {
-                const bool l1 = lane == 1;
-                const size_t di = static_cast<size_t>(l1 ? v : cur) * n + (l1 ? cur : v);
-                const size_t ci = static_cast<size_t>(cur) * 32 + static_cast<uint32_t>(pos);
-                const bool wr = lane < 2 || (lane == 2 && pos >= 0);
-                if constexpr (kAtomic) red_add_if(wr, lane < 2 ? C.cnt + di : C.cntc + ci, one);
-                else st_relaxed_if(wr, lane < 2 ? C.tau + di : C.tauc + ci, affine(tau_old, C.c_l, C.c_0));
+            // ---- off the chain: predicated stores, no shuffles.  The lane of
+            // the chosen slot writes all three copies of (cur, v) with f of the
+            // trail it scored (tau[u][v], tau[v][u], tauc[u][pos]); the lane of
+            // prev writes the late mirror copy of the previous edge; the fourth
+            // copy, tauc[v][mirror], is next step's late copy.
+            const bool me = lane == pos;
+            const size_t d_uv = static_cast<size_t>(cur) * n + v, d_vu = static_cast<size_t>(v) * n + cur;
+            if constexpr (kAtomic) {
+                red_add_if(me || mw, C.cntc + mi, one);
+                red_add_if(me, C.cnt + d_uv, one);
+                red_add_if(me, C.cnt + d_vu, one);
+            } else {
+                st_relaxed_if(me || mw, C.tauc + mi, mval);
+                st_relaxed_if(me, C.tau + d_uv, mval);
+                st_relaxed_if(me, C.tau + d_vu, mval);
             }
             mprev = cur;
             // visited mark: the winning lane stores the word it tested (pos = -1
             // after a fallback, which marked v itself)
-            sts_if(lane == pos, vw, word | bit);
+            sts_if(me, vw, word | bit);
+            lenl += me ? dl : 0;
             // RNG: commit a greedy step's q draw, peek the next one
-            if (kind == 0) rng.advance();
+            if (greedy && cand) rng.advance();
             la.prepare(rng);
-            wc.roulette += kind == 1;
-            wc.fallback += kind == 2;
-            wc.fb_elems += kind == 2 ? n - t : 0u;
-            len += d;
             route_put(route, rbuf, t, v, lane);
             cur = v;
             __syncwarp();
         }
         route_flush(route, rbuf, n - 1, lane);
         wc.updates += n - 1;
+        long long len = lenl;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) len += static_cast<long long>(shfl_xor_u64(static_cast<uint64_t>(len), o));
         // last step's late mirror copy (el/tl hold row `cur`)
         if ((el.x & kIdMask) == mprev) {
             if constexpr (kAtomic) red_add1(C.cntc + static_cast<size_t>(cur) * 32 + lane);

@@ -42,16 +42,18 @@ def main():
     ap.add_argument("libs", nargs="+")
     ap.add_argument("--variants", nargs="+", default=["atomic", "relaxed"])
     ap.add_argument("--instance", default="pr2392")
-    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--child", action="store_true")
     a = ap.parse_args()
     if a.child:
         return child(a.instance, a.variants, a.iters)
-    for lib in a.libs:
+    for spec in a.libs:  # lib[:VAR=value,...] -- e.g. base:ACS_PAIR=0
+        lib, _, extra = spec.partition(":")
         env = dict(os.environ, ACS_LIB_VARIANT="" if lib == "base" else lib)
+        env.update(kv.split("=", 1) for kv in extra.split(",") if kv)
         r = subprocess.run([sys.executable, __file__, "x", "--child", "--instance", a.instance, "--iters", str(a.iters),
                             "--variants", *a.variants], env=env, capture_output=True, text=True, timeout=900)
-        print(lib, r.stdout.strip() or r.stderr[-1500:], flush=True)
+        print(spec, r.stdout.strip() or r.stderr[-1500:], flush=True)
 
 
 if __name__ == "__main__":

@@ -202,6 +202,24 @@ def test_lean_kernel_single_ant_equals_seq(acs, orc, gpu, variant, rng, q0):
         assert cnt[k] == o[k], k
 
 
+@pytest.mark.parametrize("variant", ["atomic", "relaxed"])
+@pytest.mark.parametrize("m", [2, 3, 7, 64])
+def test_lean_kernel_small_colonies(acs, orc, gpu, variant, m):
+    """Lean kernel with small even and odd colonies: valid tours, exact
+    lengths (the per-lane length shares reduced at the tour end), exact
+    update and step counts."""
+    I = O.load("lin318")
+    with acs.Colony(to_acs(acs, I), acs.AcsParams(variant=variant, m=m, seed=m, rng="philox")) as col:
+        st = col.iterate(3)
+        routes, lens = col.routes()
+        cnt = col.counters()
+    assert_permutations(routes, I.n)
+    assert [int(x) for x in lens] == [orc.tour_length(I, r) for r in routes]
+    assert cnt["local_updates"] == 3 * m * I.n
+    assert cnt["greedy_steps"] + cnt["roulette_steps"] + cnt["fallback_steps"] == 3 * m * (I.n - 1)
+    assert st["iter_best_len"].tolist()[-1] == lens.min()
+
+
 def test_lean_kernel_single_ant_pr2392(acs, orc, gpu):
     """The headline instance through the lean kernel, one ant: bit-exact SEQ."""
     I = O.load("pr2392")
