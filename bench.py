@@ -218,7 +218,7 @@ def run_reference(args):
 def rng_for(variant: str, rng: str) -> str:
     if rng != "auto":
         return rng
-    return "philox" if variant in ("atomic", "relaxed") else "xoshiro"
+    return "philox" if variant in ("atomic", "relaxed", "spm") else "xoshiro"
 
 
 def default_q0(n: int) -> float:

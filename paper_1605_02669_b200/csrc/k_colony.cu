@@ -1090,6 +1090,218 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
     }
 }
 
+// Lean SPM records (s = 8): one 128 B line per record {vals[8] f64 | ids[8]
+// u32 | tail u32}, addressed as base + (u << 7) with constant field offsets.
+constexpr uint32_t kRec8Ids = 64, kRec8Tail = 96;
+__device__ __forceinline__ unsigned char *rec8(const DevColony &C, uint32_t u) {
+    return C.spm.base + (static_cast<size_t>(u) << 7);
+}
+__device__ __forceinline__ void st_relaxed_u32_if(bool p, uint32_t *ptr, uint32_t v) {
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.relaxed.gpu.global.b32 [%1], %2; }" ::"r"(
+                     static_cast<int>(p)),
+                 "l"(ptr), "r"(v)
+                 : "memory");
+}
+
+// One record update (D5) on the lane-distributed copy of the
+// record (lane j < 8: slot j's id and value, tail in every lane), written
+// through by lane 0 with predicated stores: hit -> the slot's value, miss ->
+// f(tau_min) into slot (tail + 1) % 8 with its id, and the tail.  kKeep: the
+// copy stays current for a following update; otherwise a hit's new value is
+// f(tau_old), the value the selection read.  Returns hit.
+template <bool kKeep>
+__device__ __forceinline__ bool spm8_update(const DevColony &C, unsigned char *rb, uint32_t nb, double tau_old,
+                                            uint32_t &idl, double &val, uint32_t &tail, int lane) {
+    const unsigned m = __ballot_sync(kFull, idl == nb);
+    const bool hit = m != 0u;
+    const uint32_t t = (tail + 1) & 7u;
+    const uint32_t slot = hit ? static_cast<uint32_t>(__ffs(m) - 1) : t;
+    const double hv = kKeep ? __shfl_sync(kFull, val, static_cast<int>(slot)) : tau_old;
+    const double y = affine(hit ? hv : C.tau_min, C.c_l, C.c_0);
+    const bool l0 = lane == 0;
+    st_relaxed_if(l0, reinterpret_cast<double *>(rb) + slot, y);
+    st_relaxed_u32_if(l0 && !hit, reinterpret_cast<uint32_t *>(rb + kRec8Ids) + slot, nb);
+    st_relaxed_u32_if(l0 && !hit, reinterpret_cast<uint32_t *>(rb + kRec8Tail), t);
+    if (kKeep) {
+        if (static_cast<uint32_t>(lane) == slot) {
+            val = y;
+            if (!hit) idl = nb;
+        }
+        if (!hit) tail = t;
+    }
+    return hit;
+}
+
+// The lean kernel's register copy of record u: the ids in every lane
+// (broadcast loads; a lane's lookup is eight compares), slot `lane`'s id and
+// value in lanes 0-7, the tail.
+struct Rec8 {
+    uint32_t id[8];
+    uint32_t idl, tail;
+    double val;
+    __device__ __forceinline__ void load(const unsigned char *rb, int lane) {
+        const uint4 q0 = __ldcg(reinterpret_cast<const uint4 *>(rb + kRec8Ids));
+        const uint4 q1 = __ldcg(reinterpret_cast<const uint4 *>(rb + kRec8Ids + 16));
+        id[0] = q0.x; id[1] = q0.y; id[2] = q0.z; id[3] = q0.w;
+        id[4] = q1.x; id[5] = q1.y; id[6] = q1.z; id[7] = q1.w;
+        val = lane < 8 ? __ldcg(reinterpret_cast<const double *>(rb) + lane) : 0.0;
+        idl = lane < 8 ? __ldcg(reinterpret_cast<const uint32_t *>(rb + kRec8Ids) + lane) : kEmpty;
+        tail = __ldcg(reinterpret_cast<const uint32_t *>(rb + kRec8Tail));
+    }
+    // first slot holding v, or -1: a depth-3 select tree over the eight
+    // (parallel) compares instead of a chain of eight selects
+    __device__ __forceinline__ int find(uint32_t v) const {
+        const int a = id[0] == v ? 0 : (id[1] == v ? 1 : -1);
+        const int b = id[2] == v ? 2 : (id[3] == v ? 3 : -1);
+        const int c = id[4] == v ? 4 : (id[5] == v ? 5 : -1);
+        const int d = id[6] == v ? 6 : (id[7] == v ? 7 : -1);
+        const int ab = a >= 0 ? a : b, cd = c >= 0 ? c : d;
+        return ab >= 0 ? ab : cd;
+    }
+};
+
+// SPM for the paper's configuration (k = 1, 32-slot lists, s = 8 slots): the
+// lean step of k_tour_lean over the selective memory.  Record cur owes two
+// ordered updates in a step (D4): the second half of the previous edge
+// (neighbour prev), then the first half of this edge (neighbour v).  Both are
+// applied after the next row's loads.  The selection reads the record as it
+// will be after the first one: only an unvisited candidate's value matters,
+// prev is visited, so the only effect is a miss evicting slot (tail + 1) % S.
+#ifndef ACS_SPM_REGS
+#define ACS_SPM_REGS 96
+#endif
+// 96 registers: 5 warps per SM sub-partition (16K registers each), so m = n = 2392 is one wave
+template <class RNG>
+__global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C) {
+    constexpr int S = 8;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
+    uint32_t *vis = reinterpret_cast<uint32_t *>(smem + wpb * 32 * sizeof(double)) + static_cast<size_t>(wib) * I.words;
+    const uint64_t it = *C.iter;
+    const uint32_t n = I.n;
+    WarpCounters wc;
+
+    for (uint32_t a = blockIdx.x * wpb + wib; a < C.m; a += gridDim.x * wpb) {
+        for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
+        RNG rng;
+        rng_init(rng, C, it, a);
+        const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));
+        uint4 el = __ldg(C.rows + static_cast<size_t>(start) * 32 + lane);
+        Rec8 rec;
+        rec.load(rec8(C, start), lane);
+        __syncwarp();
+        if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
+        __syncwarp();
+        uint32_t *route = C.routes + static_cast<size_t>(a) * n;
+        uint32_t rbuf = start, cur = start, prev = kEmpty;  // kEmpty: no pending update yet
+        long long lenl = 0;
+        Lookahead<RNG> la;
+        la.prepare(rng);
+
+        for (uint32_t t = 1; t < n; ++t) {
+            const uint32_t c = el.x & kIdMask;
+            uint32_t *vw = vis + (c >> 5);
+            const uint32_t word = *vw, bit = 1u << (c & 31);
+            const bool unv = !(word & bit);
+            // pending update of record cur with prev: a miss evicts slot (tail+1) % S
+            const bool pend = prev != kEmpty;
+            const bool pmiss = pend && __ballot_sync(kFull, rec.idl == prev) == 0u;
+            const int evict = pmiss ? static_cast<int>((rec.tail + 1) & 7u) : -1;
+            int hit = rec.find(c);
+            if (hit == evict) hit = -1;
+            const double hv = __shfl_sync(kFull, rec.val, hit < 0 ? 0 : hit);
+            const double tv = hit < 0 ? C.tau_min : hv;
+            const double score = __dmul_rn(tv, __hiloint2double(static_cast<int>(el.w), static_cast<int>(el.z)));
+            const int32_t dl = static_cast<int32_t>(el.y);
+            int pos;
+            uint32_t v;
+            bool cand;
+            const bool greedy = la.greedy(C);
+            if (greedy) {
+                cand = warp_argmax_id(score, unv, c, lane, pos, v);
+            } else {
+                const unsigned um = __ballot_sync(kFull, unv);
+                cand = um != 0u;
+                if (cand) {
+                    rng.advance();  // commit q (P1)
+                    const double r = uniform01(rng);
+                    pos = warp_roulette_pos(unv ? score : 0.0, um, r, scratch, lane);
+                    v = __shfl_sync(kFull, c, pos);
+                    ++wc.roulette;
+                }
+            }
+            double tau_old = 0.0;
+            if (!cand) {  // fallback: the record after its pending update, then the scan
+                if (pend) {
+                    wc.misses += !spm8_update<true>(C, rec8(C, cur), prev, 0.0, rec.idl, rec.val, rec.tail, lane);
+                    prev = kEmpty;
+                }
+                Step st;
+                fallback_scan(I, C, vis, cur,
+                              [&](uint32_t x, bool act) {  // all lanes call: the value comes by shuffle
+                                  const int j = act ? rec.find(x) : -1;
+                                  const double y = __shfl_sync(kFull, rec.val, j < 0 ? 0 : j);
+                                  return j < 0 ? C.tau_min : y;
+                              },
+                              lane, st);
+                v = st.v;
+                pos = -1;
+                tau_old = st.tau_old;
+                if (lane == 0) {
+                    vis[v >> 5] |= 1u << (v & 31);
+                    lenl += st.d;
+                }
+                ++wc.fallback;
+                wc.fb_elems += n - t;
+            } else {
+                tau_old = __shfl_sync(kFull, tv, pos);
+            }
+            // record cur's lane-distributed slots: all its two updates need
+            uint32_t ridl = rec.idl, rtail = rec.tail;
+            double rval = rec.val;
+            // ---- next row and record: issued as soon as v is known
+            el = __ldg(C.rows + static_cast<size_t>(v) * 32 + lane);
+            rec.load(rec8(C, v), lane);
+            // ---- off the chain: record cur's two ordered updates
+            // (hits are derived at the tour end: 2 record operations per update)
+            unsigned char *rb = rec8(C, cur);
+            if (prev != kEmpty) wc.misses += !spm8_update<true>(C, rb, prev, 0.0, ridl, rval, rtail, lane);
+            wc.misses += !spm8_update<false>(C, rb, v, tau_old, ridl, rval, rtail, lane);
+            prev = cur;
+            const bool me = lane == pos;
+            sts_if(me, vw, word | bit);
+            lenl += me ? dl : 0;
+            if (greedy && cand) rng.advance();
+            la.prepare(rng);
+            route_put(route, rbuf, t, v, lane);
+            cur = v;
+            __syncwarp();
+        }
+        route_flush(route, rbuf, n - 1, lane);
+        wc.updates += n - 1;
+        long long len = lenl;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) len += static_cast<long long>(shfl_xor_u64(static_cast<uint64_t>(len), o));
+        // record cur's pending update, then the closing edge: record last, then record start
+        unsigned char *rb = rec8(C, cur);
+        if (prev != kEmpty) wc.misses += !spm8_update<true>(C, rb, prev, 0.0, rec.idl, rec.val, rec.tail, lane);
+        const int32_t dclose = tsplib_distance(I.type, __ldg(I.xs + cur), __ldg(I.ys + cur), __ldg(I.xs + start),
+                                               __ldg(I.ys + start));
+        ++wc.updates;
+        wc.misses += !spm8_update<true>(C, rb, start, 0.0, rec.idl, rec.val, rec.tail, lane);
+        __syncwarp();
+        Rec8 r2;
+        r2.load(rec8(C, start), lane);
+        wc.misses += !spm8_update<true>(C, rec8(C, start), cur, 0.0, r2.idl, r2.val, r2.tail, lane);
+        wc.hits = 2 * n - wc.misses;  // n local updates (k = 1), two record operations each
+        if (lane == 0) C.lens[a] = len + dclose;
+        wc.flush(C.counters, lane, n - 1);
+        __syncwarp();
+    }
+}
+
 // ============================================================ deferred (SYNC)
 
 // Grid-wide barrier of the cooperative (all-CTAs-resident) deferred kernel.
@@ -1860,7 +2072,13 @@ static void launch_spm_rng(const DevInstance &I, const DevColony &C, bool one_wa
         case 2: launch_tour_kernel(k_construct_spm<2, RNG>, I, C, one_warp, s); break;
         case 4: launch_tour_kernel(k_construct_spm<4, RNG>, I, C, one_warp, s); break;
         case 8:
-            if (C.k == 1 && C.L == 32 && !one_warp) launch_tour_kernel(k_construct_spm<8, RNG, true>, I, C, false, s);
+            if (C.k == 1 && C.L == 32 && !one_warp) {
+#ifdef ACS_X_OLD_SPM
+                launch_tour_kernel(k_construct_spm<8, RNG, true>, I, C, false, s);
+#else
+                launch_tour_kernel(k_spm_lean<RNG>, I, C, false, s);
+#endif
+            }
             else launch_tour_kernel(k_construct_spm<8, RNG>, I, C, one_warp, s);
             break;
         default: launch_tour_kernel(k_construct_spm<16, RNG>, I, C, one_warp, s); break;

@@ -23,7 +23,7 @@ def child(instance, variants, iters):
     out = {}
     for v in variants:
         for m in (inst.n, 128):
-            rng = "philox" if v in ("atomic", "relaxed") else "xoshiro"
+            rng = "philox" if v in ("atomic", "relaxed", "spm") else "xoshiro"
             with P.Colony(inst, P.AcsParams(variant=v, m=m, seed=1, rng=rng)) as col:
                 col.iterate(3)
                 ms = []

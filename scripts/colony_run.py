@@ -16,7 +16,7 @@ ap.add_argument("--instance", default="pr2392")
 ap.add_argument("--rng", default="auto")
 a = ap.parse_args()
 inst = P.load_instance(a.instance)
-rng = a.rng if a.rng != "auto" else ("philox" if a.variant in ("atomic", "relaxed") else "xoshiro")
+rng = a.rng if a.rng != "auto" else ("philox" if a.variant in ("atomic", "relaxed", "spm") else "xoshiro")
 with P.Colony(inst, P.AcsParams(variant=a.variant, m=a.ants or inst.n, seed=1, rng=rng)) as col:
     for _ in range(a.iters):
         col.iterate(1)

@@ -202,7 +202,31 @@ def test_lean_kernel_single_ant_equals_seq(acs, orc, gpu, variant, rng, q0):
         assert cnt[k] == o[k], k
 
 
-@pytest.mark.parametrize("variant", ["atomic", "relaxed"])
+@pytest.mark.parametrize("rng", ["xoshiro", "philox"])
+@pytest.mark.parametrize("q0", [-1.0, 0.0, 0.7])
+@pytest.mark.parametrize("name", ["d198", "pcb442"])
+def test_spm_lean_single_ant_equals_seq(acs, orc, gpu, rng, q0, name):
+    """k = 1, 32-slot lists, s = 8 runs the lean SPM kernel (k_spm_lean): with
+    one ant it must reproduce SEQ x SELECTIVE bit for bit -- the records
+    (ids, values, tails), routes, trace and the hit / miss counts."""
+    I = O.load(name)
+    p = acs.AcsParams(variant="spm", m=1, seed=5, rng=rng, q0=q0)
+    with acs.Colony(to_acs(acs, I), p) as col:
+        st = col.iterate(5)
+        ids, vals, tail = col.selective()
+        routes, lens = col.routes()
+        cnt = col.counters()
+    o = orc.run(I, m=1, iterations=5, seed=5, mode=O.SEQ, memory=O.SELECTIVE, want_spm=True, q0=q0,
+                rng=O.PHILOX if rng == "philox" else O.XOSHIRO)
+    assert st["global_best_len"].tolist() == o["trace"].tolist()
+    assert (routes == o["routes"]).all() and lens.tolist() == o["lengths"].tolist()
+    assert (ids == o["spm_ids"]).all() and (tail == o["spm_tail"]).all()
+    assert np.array_equal(vals.view(np.uint64), o["spm_vals"].view(np.uint64))
+    for k in ("hits", "misses", "fallback_steps", "greedy_steps", "roulette_steps", "local_updates"):
+        assert cnt[k] == o[k], k
+
+
+@pytest.mark.parametrize("variant", ["atomic", "relaxed", "spm"])
 @pytest.mark.parametrize("m", [2, 3, 7, 64])
 def test_lean_kernel_small_colonies(acs, orc, gpu, variant, m):
     """Lean kernel with small even and odd colonies: valid tours, exact
