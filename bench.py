@@ -133,6 +133,18 @@ def resident_ants(P, device: int, m: int) -> int:
     return sms * 20 if m <= sms * 20 else sms * 28
 
 
+def construct_kernel(variant: str, k: int) -> str:
+    """The construction kernel the library launches for this workload (cl = 32)."""
+    if variant == "deferred":
+        return "k_deferred"
+    if variant == "spm-sync":
+        return "k_ssync_select"
+    lean = k == 1
+    if variant in ("spm", "spm-seq"):
+        return "k_spm_lean" if lean and variant == "spm" else "k_construct_spm"
+    return "k_tour_lean" if lean and variant in ("atomic", "relaxed") else "k_construct_dense"
+
+
 def measured_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -361,7 +373,7 @@ def main():
                                 "is L2-resident, so DRAM traffic is the cold fill only",
                 "peak_source": "acs_gpu_l2_read_bandwidth: ld.global.cg stream over a 48 MiB L2-resident "
                                "buffer, measured in this run",
-                "kernel": "k_construct_dense" if args.variant not in ("spm",) else "k_construct_spm",
+                "kernel": construct_kernel(args.variant, args.k),
                 "construct_ms_per_launch": round(construct_s * 1e3, 4),
                 "bytes_per_tour": B_tour,
                 "algorithmic_bytes_per_launch": round(alg_bytes_launch),
