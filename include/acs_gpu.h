@@ -27,8 +27,9 @@
 extern "C" {
 #endif
 
-#define ACS_GPU_ABI_VERSION 4  /* 2: acs_counters.fallback_full, acs_random_instance; 3: ACS_VARIANT_SPM_SYNC;
-                                  4: acs_gpu_island_exchange_local, acs_gpu_l2_latency, 16-bit island ranks */
+#define ACS_GPU_ABI_VERSION 5  /* 2: acs_counters.fallback_full, acs_random_instance; 3: ACS_VARIANT_SPM_SYNC;
+                                  4: acs_gpu_island_exchange_local, acs_gpu_l2_latency, 16-bit island ranks;
+                                  5: acs_counters.relaxed_writes / lost_updates */
 
 /* status codes */
 #define ACS_OK 0
@@ -93,6 +94,10 @@ typedef struct {
     uint64_t iterations;     /* iterations run on this context */
     uint64_t fallback_elems; /* unvisited nodes a full fallback scan covers (algorithmic) */
     uint64_t fallback_full;  /* fallback steps the pruned pass could not settle (full scan run) */
+    /* RELAXED lost-update instrumentation (library built with -DACS_COUNT_LOST, else 0):
+     * pheromone writes of the relaxed construction, and those that replaced a value
+     * other than the one their update read (another ant's update was lost) */
+    uint64_t relaxed_writes, lost_updates;
 } acs_counters;
 
 typedef struct {

@@ -26,6 +26,14 @@ __device__ __forceinline__ int32_t dist_of(const DevInstance &I, uint32_t u, uin
     return tsplib_distance(I.type, xu, yu, __ldg(I.xs + v), __ldg(I.ys + v));
 }
 
+// eta^beta of distance d: repeated multiply for integral beta (P2), the
+// host-built distance table otherwise (DevInstance::eta_d)
+__device__ __forceinline__ double eta_beta_i(const DevInstance &I, int32_t d, double beta, int beta_int) {
+    if (beta_int >= 0 || !I.eta_d) return eta_beta(d, beta, beta_int);
+    const uint32_t k = static_cast<uint32_t>(d > 0 ? d : 0);
+    return __ldg(I.eta_d + (k < I.eta_dmax ? k : I.eta_dmax));
+}
+
 __device__ __forceinline__ bool visited(const uint32_t *vis, uint32_t v) {
     return (vis[v >> 5] >> (v & 31)) & 1u;
 }

@@ -51,6 +51,11 @@ struct DevInstance {
     const double *xs, *ys;
     const int32_t *dist; // n*n or nullptr (on-the-fly above 4096 nodes)
     const double *etab;  // n*n eta^beta (fallback scan operand) or nullptr
+    // non-integral beta: eta^beta by integer distance d (0..eta_dmax), built on
+    // the host with the C library's pow -- the value the oracle computes -- so
+    // every eta^beta on the device is bit-identical to it; nullptr otherwise
+    const double *eta_d;
+    uint32_t eta_dmax;
 };
 
 constexpr uint32_t kHot = 32;  // hot-list entries per row (one per lane)
@@ -85,7 +90,8 @@ struct DevColony {
 
 enum Counter {
     kCntUpdates = 0, kCntHits, kCntMisses, kCntFallback, kCntGreedy, kCntRoulette,
-    kCntCasRetry, kCntIters, kCntFallbackElems, kCntFallbackFull, kNumCounters = 16
+    kCntCasRetry, kCntIters, kCntFallbackElems, kCntFallbackFull, kCntRelaxedWrites, kCntLost,
+    kNumCounters = 16
 };
 
 struct DevBest {
@@ -107,6 +113,8 @@ struct DevSpmSync {
 
 struct DevDeferred {
     uint32_t ants_per_warp;    // set by the launcher (grid barrier: cooperative groups)
+    unsigned long long *cell;  // n*n pending cells of tau: acc | s0 << 32 | s1 << 48 (k_deferred2)
+    unsigned long long *cellc; // n*32 pending cells of tauc
 };
 
 // ---- setup launchers (stream-ordered, async) ----

@@ -135,6 +135,8 @@ struct DevInst {
         view.ys = ys.p;
         view.dist = nullptr;
         view.etab = nullptr;
+        view.eta_d = nullptr;
+        view.eta_dmax = 0;
         if (want_table && n <= 4096) {  // tsp_instance.hpp:31 kDistTableMaxNodes
             CUDA_TRY(dist.alloc(static_cast<size_t>(n) * n));
             launch_distance_table(view, dist.p, s);
@@ -212,9 +214,11 @@ struct acs_gpu_ctx {
     DBuf<uint32_t> hot, hot_cnt;  // per-row non-candidate edges the global update touched
     DBuf<uint32_t> cand;  // flat n*L (reference layout), kept for get_candidates
     DBuf<double> tau, tauc, etab, pw;
+    DBuf<double> eta_d;  // non-integral beta: eta^beta by integer distance
     DBuf<unsigned char> spm;   // record-major selective memory (SpmMem)
     SpmMem spm_mem;
     DBuf<uint32_t> cnt, cntc;  // ATOMIC variant: pending local updates per copy
+    DBuf<unsigned long long> dcell, dcellc;  // DEFERRED: pending cells (acc | step parity slots)
     DBuf<uint32_t> routes, best_tour;
     DBuf<int64_t> lens, best_len;
     DBuf<uint64_t> iter;
@@ -259,7 +263,8 @@ struct acs_gpu_ctx {
     size_t device_bytes() const {
         return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + etab.bytes() + rows.bytes() + ext.bytes() + hot.bytes() + hot_cnt.bytes() + cand.bytes() +
                tau.bytes() + tauc.bytes() + spm.bytes() +
-               routes.bytes() + best_tour.bytes() + lens.bytes() + cnt.bytes() + cntc.bytes();
+               routes.bytes() + best_tour.bytes() + lens.bytes() + cnt.bytes() + cntc.bytes() + dcell.bytes() +
+               dcellc.bytes();
     }
 };
 
@@ -589,6 +594,26 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     const DevInstance &I = c->inst.view;
     const uint32_t n = c->n;
     const int bint = beta_int_of(p->beta);
+    if (bint < 0) {
+        // non-integral beta: eta^beta per integer distance, host pow (bit-identical
+        // to the oracle's), bounded by the bounding-box diagonal
+        double x0 = inst->xs[0], x1 = x0, y0 = inst->ys[0], y1 = y0;
+        for (uint32_t i = 1; i < n; ++i) {
+            x0 = std::min(x0, inst->xs[i]); x1 = std::max(x1, inst->xs[i]);
+            y0 = std::min(y0, inst->ys[i]); y1 = std::max(y1, inst->ys[i]);
+        }
+        double diag = std::sqrt((x1 - x0) * (x1 - x0) + (y1 - y0) * (y1 - y0));
+        if (inst->edge_weight_type == ACS_ATT) diag = diag / std::sqrt(10.0);
+        if (!(diag < 1e9)) return fail(ACS_E_ARG, "non-integral beta: coordinate range too large for the eta^beta table");
+        const uint32_t dmax = static_cast<uint32_t>(std::ceil(diag)) + 2;
+        std::vector<double> tab(static_cast<size_t>(dmax) + 1);
+        for (uint32_t d = 0; d <= dmax; ++d) tab[d] = std::pow(1.0 / static_cast<double>(d > 0 ? d : 1), p->beta);
+        CUDA_TRY(c->eta_d.alloc(tab.size()));
+        CUDA_TRY(cudaMemcpyAsync(c->eta_d.p, tab.data(), c->eta_d.bytes(), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));  // the host table dies with this scope
+        c->inst.view.eta_d = c->eta_d.p;
+        c->inst.view.eta_dmax = dmax;
+    }
 
     // candidate lists (K2) + packed rows
     CUDA_TRY(c->cand.alloc(static_cast<size_t>(n) * c->L));
@@ -674,7 +699,13 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     CUDA_TRY(cudaMemcpyAsync(c->best_len.p, &none, sizeof(int64_t), cudaMemcpyHostToDevice, s));
 
     if (p->variant == ACS_VARIANT_DEFERRED) {
-        c->deferred = DevDeferred{1};
+        // the pending cells count one step's updates of a copy in 16 bits
+        if (c->m > 65535) return fail(ACS_E_ARG, "deferred (SYNC) variant supports m <= 65535");
+        CUDA_TRY(c->dcell.alloc(static_cast<size_t>(n) * n));
+        CUDA_TRY(c->dcellc.alloc(static_cast<size_t>(n) * 32));
+        CUDA_TRY(cudaMemsetAsync(c->dcell.p, 0, c->dcell.bytes(), s));
+        CUDA_TRY(cudaMemsetAsync(c->dcellc.p, 0, c->dcellc.bytes(), s));
+        c->deferred = DevDeferred{1, c->dcell.p, c->dcellc.p};
     }
     if (p->variant == ACS_VARIANT_SPM_SYNC) {
         // the apply pass sorts the step's 2m ops in one CTA's shared memory
@@ -899,6 +930,8 @@ int acs_gpu_get_counters(const acs_gpu_ctx *c, acs_counters *o) {
     o->iterations = h[kCntIters];
     o->fallback_elems = h[kCntFallbackElems];
     o->fallback_full = h[kCntFallbackFull];
+    o->relaxed_writes = h[kCntRelaxedWrites];
+    o->lost_updates = h[kCntLost];
     return ACS_OK;
 }
 

@@ -126,7 +126,7 @@ __global__ void k_ext_rows(DevInstance I, const uint32_t *cand, uint32_t L, cons
     uint4 el = make_uint4(kEmpty, 0u, 0u, 0u);
     if (key != ~0ull) {
         const int32_t d = static_cast<int32_t>(key >> 32);
-        const uint64_t b = dbits(eta_beta(d, beta, beta_int));
+        const uint64_t b = dbits(eta_beta_i(I, d, beta, beta_int));
         const uint32_t v = static_cast<uint32_t>(key);
         uint32_t mirror = kNoMirror;
         for (uint32_t q = 0; q < L; ++q)
@@ -148,7 +148,7 @@ __global__ void k_build_rows(DevInstance I, const uint32_t *cand, uint32_t L, do
     if (p < L) {
         const uint32_t c = cand[static_cast<size_t>(u) * L + p];
         const int32_t d = tsplib_distance(I.type, I.xs[u], I.ys[u], I.xs[c], I.ys[c]);
-        const double eb = eta_beta(d, beta, beta_int);
+        const double eb = eta_beta_i(I, d, beta, beta_int);
         uint32_t mirror = kNoMirror;
         for (uint32_t q = 0; q < L; ++q)
             if (cand[static_cast<size_t>(c) * L + q] == u) { mirror = q; break; }
@@ -274,7 +274,7 @@ __global__ void k_eta_table(DevInstance I, double beta, int beta_int, double *ou
     if (v >= I.n) return;
     const int32_t d = tsplib_distance(I.type, __ldg(I.xs + u), __ldg(I.ys + u), __ldg(I.xs + v),
                                       __ldg(I.ys + v));
-    out[static_cast<size_t>(u) * I.n + v] = eta_beta(d, beta, beta_int);
+    out[static_cast<size_t>(u) * I.n + v] = eta_beta_i(I, d, beta, beta_int);
 }
 
 __global__ void k_spm_script(SpmMem M, double tau_min, double c_l, double c_0, double alpha, double c_g,

@@ -307,3 +307,81 @@ def test_spm_sync_slots_bit_exact(acs, orc, gpu, slots):
     I = O.load("d198")
     r = pair(acs, orc, I, "sync", O.SELECTIVE, m=198, iters=3, seed=6, s=slots)
     check_exact(*r, O.SELECTIVE)
+
+
+@pytest.mark.parametrize("name,m", [("d198", 198), ("pcb442", 442)])
+def test_atomic_fold_matches_sequential_updates(acs, orc, gpu, name, m):
+    """ATOMIC (CONSISTENT) after one iteration: every copy of edge {u, v} was
+    bumped once per ant that traversed it, and the epilogue folds c pending
+    updates into the base (k_fold_counts / trail_value): the affine rule
+    itself for c <= 1, the closed form tau_min + c_l^c (b - tau_min) for
+    c >= 2.  The folded matrix must equal f applied c times in sequence (c
+    from the routes) within 1e-12 relative, and bit for bit where c <= 1.
+    The global update then touches only the best tour's edges."""
+    I = O.load(name)
+    rho, alpha = 0.01, 0.2
+    with acs.Colony(to_acs(acs, I), acs.AcsParams(variant="atomic", m=m, seed=4, rho=rho, alpha=alpha)) as col:
+        col.iterate(1)
+        tau = col.pheromone()
+        routes, _ = col.routes()
+        best, blen = col.best()
+        tau0 = col.info.tau0
+    n = I.n
+    c = np.zeros((n, n), np.int64)
+    for r in routes.astype(np.int64):
+        u, v = r, np.roll(r, -1)
+        np.add.at(c, (u, v), 1)
+        np.add.at(c, (v, u), 1)
+    c_orig = c.copy()
+    # f^c(tau0), sequential, with the device's constants
+    c_l, c_0 = 1.0 - rho, rho * tau0
+    want = np.full((n, n), tau0)
+    for _ in range(int(c.max())):
+        step = c > 0
+        want[step] = c_l * want[step] + c_0
+        c[step] -= 1
+    bu = best.astype(np.int64)
+    gb = np.zeros((n, n), bool)
+    gb[bu, np.roll(bu, -1)] = True
+    gb[np.roll(bu, -1), bu] = True
+    keep = ~gb
+    rel = np.abs(tau[keep] - want[keep]) / want[keep]
+    assert rel.max() < 1e-12, rel.max()
+    low = keep & (c_orig <= 1)
+    assert np.array_equal(tau[low].view(np.uint64), want[low].view(np.uint64))
+    assert (c_orig[keep] >= 2).any()  # the closed form was exercised
+    # the global update on the best tour's edges: tau' = (1 - alpha) tau_folded + alpha / L_gb
+    c_d = alpha * (1.0 / blen)
+    g = (1.0 - alpha) * want[gb] + c_d
+    assert (np.abs(tau[gb] - g) / g).max() < 1e-12
+
+
+@pytest.mark.parametrize("beta", [2.5, 0.7])
+@pytest.mark.parametrize("mode,memory", MODES)
+def test_non_integer_beta_bit_exact(acs, orc, gpu, beta, mode, memory):
+    """a non-integral beta takes eta^beta from a table by integer
+    distance built on the host with the C library's pow -- the oracle's own
+    computation -- so the deterministic variants stay bit-exact."""
+    I = O.load("d198")
+    r = pair(acs, orc, I, mode, memory, m=24, iters=3, beta=beta, seed=6)
+    check_exact(*r, memory)
+
+
+def test_non_integer_beta_no_eta_table(acs, orc, gpu):
+    """n > 4096 (no eta^beta matrix: the fallback computes distances on the fly)
+    with a non-integral beta, through the distance table."""
+    I = small_instance(4200, seed=5, scale=20000)
+    r = pair(acs, orc, I, "seq", O.DENSE, m=3, iters=1, beta=1.5, seed=2, q0=0.5)
+    check_exact(*r, O.DENSE)
+
+
+def test_non_integer_beta_lean_kernel(acs, orc, gpu):
+    """The lean kernel (k = 1, 32-slot lists) with beta = 2.5, one ant: SEQ."""
+    I = O.load("pcb442")
+    p = acs.AcsParams(variant="relaxed", m=1, seed=3, beta=2.5, rng="philox")
+    with acs.Colony(to_acs(acs, I), p) as col:
+        st = col.iterate(3)
+        tau = col.pheromone()
+    o = orc.run(I, m=1, iterations=3, seed=3, mode=O.SEQ, want_tau=True, beta=2.5, rng=O.PHILOX)
+    assert st["global_best_len"].tolist() == o["trace"].tolist()
+    assert np.array_equal(tau.view(np.uint64), o["tau"].view(np.uint64))

@@ -33,7 +33,7 @@ def test_every_header_symbol_is_exported(acs):
     assert not missing, f"not exported: {missing}"
     from paper_1605_02669_b200 import _native as N
     assert set(N.SIGNATURES) == set(names)
-    assert acs.lib().acs_gpu_abi_version() == 4
+    assert acs.lib().acs_gpu_abi_version() == 5
 
 
 def test_library_is_sm100a(acs):
