@@ -29,7 +29,7 @@ extern "C" {
 
 #define ACS_GPU_ABI_VERSION 5  /* 2: acs_counters.fallback_full, acs_random_instance; 3: ACS_VARIANT_SPM_SYNC;
                                   4: acs_gpu_island_exchange_local, acs_gpu_l2_latency, 16-bit island ranks;
-                                  5: acs_counters.relaxed_writes / lost_updates */
+                                  5: acs_counters.relaxed_writes / lost_updates / fallback_grid */
 
 /* status codes */
 #define ACS_OK 0
@@ -95,9 +95,11 @@ typedef struct {
     uint64_t fallback_elems; /* unvisited nodes a full fallback scan covers (algorithmic) */
     uint64_t fallback_full;  /* fallback steps the pruned pass could not settle (full scan run) */
     /* RELAXED lost-update instrumentation (library built with -DACS_COUNT_LOST, else 0):
-     * pheromone writes of the relaxed construction, and those that replaced a value
-     * other than the one their update read (another ant's update was lost) */
+     * candidate-copy pheromone writes of the relaxed construction, and those that
+     * replaced a value other than the one their update read (another ant's update
+     * of that trail landed in between and was lost) */
     uint64_t relaxed_writes, lost_updates;
+    uint64_t fallback_grid;  /* fallback steps settled by the grid-ring walk past the ext rows (n > 4096) */
 } acs_counters;
 
 typedef struct {

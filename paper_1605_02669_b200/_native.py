@@ -47,7 +47,8 @@ class Counters(C.Structure):
                 ("fallback_steps", C.c_uint64), ("greedy_steps", C.c_uint64),
                 ("roulette_steps", C.c_uint64), ("cas_retries", C.c_uint64),
                 ("iterations", C.c_uint64), ("fallback_elems", C.c_uint64),
-                ("fallback_full", C.c_uint64), ("relaxed_writes", C.c_uint64), ("lost_updates", C.c_uint64)]
+                ("fallback_full", C.c_uint64), ("relaxed_writes", C.c_uint64), ("lost_updates", C.c_uint64),
+                ("fallback_grid", C.c_uint64)]
 
 
 class CtxInfo(C.Structure):

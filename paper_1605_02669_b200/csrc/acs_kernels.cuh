@@ -86,12 +86,18 @@ struct DevColony {
     int64_t *lens;         // m
     unsigned long long *counters;  // [8], see Counter
     const uint64_t *iter;  // device iteration counter (RNG derivation index)
+    // uniform grid over the bounding box (n > 4096, EUC_2D / CEIL_2D): the
+    // pruned fallback continues past the ext rows ring by ring of cells
+    const uint32_t *cell_start;  // g*g + 1 (CSR), or nullptr
+    const uint32_t *cell_nodes;  // n node ids, by cell then id
+    uint32_t grid_g;
+    double grid_x0, grid_y0, grid_h;
 };
 
 enum Counter {
     kCntUpdates = 0, kCntHits, kCntMisses, kCntFallback, kCntGreedy, kCntRoulette,
     kCntCasRetry, kCntIters, kCntFallbackElems, kCntFallbackFull, kCntRelaxedWrites, kCntLost,
-    kNumCounters = 16
+    kCntFallbackGrid, kNumCounters = 16
 };
 
 struct DevBest {
@@ -113,8 +119,6 @@ struct DevSpmSync {
 
 struct DevDeferred {
     uint32_t ants_per_warp;    // set by the launcher (grid barrier: cooperative groups)
-    unsigned long long *cell;  // n*n pending cells of tau: acc | s0 << 32 | s1 << 48 (k_deferred2)
-    unsigned long long *cellc; // n*32 pending cells of tauc
 };
 
 // ---- setup launchers (stream-ordered, async) ----

@@ -7,6 +7,7 @@
 
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <memory>
@@ -212,13 +213,13 @@ struct acs_gpu_ctx {
     int64_t nn_len = 0;
     DBuf<uint4> rows, ext;     // candidate rows; next-nearest rows for the pruned fallback
     DBuf<uint32_t> hot, hot_cnt;  // per-row non-candidate edges the global update touched
+    DBuf<uint32_t> cell_start, cell_nodes;  // uniform grid (CSR) for the fallback beyond the ext rows
     DBuf<uint32_t> cand;  // flat n*L (reference layout), kept for get_candidates
     DBuf<double> tau, tauc, etab, pw;
     DBuf<double> eta_d;  // non-integral beta: eta^beta by integer distance
     DBuf<unsigned char> spm;   // record-major selective memory (SpmMem)
     SpmMem spm_mem;
     DBuf<uint32_t> cnt, cntc;  // ATOMIC variant: pending local updates per copy
-    DBuf<unsigned long long> dcell, dcellc;  // DEFERRED: pending cells (acc | step parity slots)
     DBuf<uint32_t> routes, best_tour;
     DBuf<int64_t> lens, best_len;
     DBuf<uint64_t> iter;
@@ -261,10 +262,9 @@ struct acs_gpu_ctx {
         return ACS_OK;
     }
     size_t device_bytes() const {
-        return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + etab.bytes() + rows.bytes() + ext.bytes() + hot.bytes() + hot_cnt.bytes() + cand.bytes() +
+        return inst.xs.bytes() + inst.ys.bytes() + inst.dist.bytes() + etab.bytes() + rows.bytes() + ext.bytes() + hot.bytes() + hot_cnt.bytes() + cell_start.bytes() + cell_nodes.bytes() + cand.bytes() +
                tau.bytes() + tauc.bytes() + spm.bytes() +
-               routes.bytes() + best_tour.bytes() + lens.bytes() + cnt.bytes() + cntc.bytes() + dcell.bytes() +
-               dcellc.bytes();
+               routes.bytes() + best_tour.bytes() + lens.bytes() + cnt.bytes() + cntc.bytes();
     }
 };
 
@@ -699,13 +699,7 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     CUDA_TRY(cudaMemcpyAsync(c->best_len.p, &none, sizeof(int64_t), cudaMemcpyHostToDevice, s));
 
     if (p->variant == ACS_VARIANT_DEFERRED) {
-        // the pending cells count one step's updates of a copy in 16 bits
-        if (c->m > 65535) return fail(ACS_E_ARG, "deferred (SYNC) variant supports m <= 65535");
-        CUDA_TRY(c->dcell.alloc(static_cast<size_t>(n) * n));
-        CUDA_TRY(c->dcellc.alloc(static_cast<size_t>(n) * 32));
-        CUDA_TRY(cudaMemsetAsync(c->dcell.p, 0, c->dcell.bytes(), s));
-        CUDA_TRY(cudaMemsetAsync(c->dcellc.p, 0, c->dcellc.bytes(), s));
-        c->deferred = DevDeferred{1, c->dcell.p, c->dcellc.p};
+        c->deferred = DevDeferred{1};
     }
     if (p->variant == ACS_VARIANT_SPM_SYNC) {
         // the apply pass sorts the step's 2m ops in one CTA's shared memory
@@ -739,6 +733,39 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
         CUDA_TRY(cudaMemsetAsync(c->hot_cnt.p, 0, n * sizeof(uint32_t), s));
         C.hot = c->hot.p;
         C.hot_cnt = c->hot_cnt.p;
+        // without an eta^beta table (n > 4096) a fallback the ext rows cannot
+        // settle continues over a uniform grid, about two nodes per cell
+        if (!I.etab && I.type != ACS_ATT && !std::getenv("ACS_NO_GRID")) {
+            double x0 = inst->xs[0], x1 = x0, y0 = inst->ys[0], y1 = y0;
+            for (uint32_t i = 1; i < n; ++i) {
+                x0 = std::min(x0, inst->xs[i]); x1 = std::max(x1, inst->xs[i]);
+                y0 = std::min(y0, inst->ys[i]); y1 = std::max(y1, inst->ys[i]);
+            }
+            const uint32_t g = std::max<uint32_t>(1, static_cast<uint32_t>(std::ceil(std::sqrt(n / 2.0))));
+            const double w = std::max(x1 - x0, y1 - y0);
+            const double h = w > 0 ? w / g : 1.0;
+            auto cell_of = [&](uint32_t i) {
+                const uint32_t cx = std::min<uint32_t>(g - 1, static_cast<uint32_t>((inst->xs[i] - x0) / h));
+                const uint32_t cy = std::min<uint32_t>(g - 1, static_cast<uint32_t>((inst->ys[i] - y0) / h));
+                return cy * g + cx;
+            };
+            std::vector<uint32_t> start(static_cast<size_t>(g) * g + 1, 0), nodes(n);
+            for (uint32_t i = 0; i < n; ++i) ++start[cell_of(i) + 1];
+            for (size_t k = 1; k < start.size(); ++k) start[k] += start[k - 1];
+            std::vector<uint32_t> fill(start.begin(), start.end() - 1);
+            for (uint32_t i = 0; i < n; ++i) nodes[fill[cell_of(i)]++] = i;  // ascending id within a cell
+            CUDA_TRY(c->cell_start.alloc(start.size()));
+            CUDA_TRY(c->cell_nodes.alloc(n));
+            CUDA_TRY(cudaMemcpyAsync(c->cell_start.p, start.data(), c->cell_start.bytes(), cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(c->cell_nodes.p, nodes.data(), c->cell_nodes.bytes(), cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            C.cell_start = c->cell_start.p;
+            C.cell_nodes = c->cell_nodes.p;
+            C.grid_g = g;
+            C.grid_x0 = x0;
+            C.grid_y0 = y0;
+            C.grid_h = h;
+        }
     }
     C.tau = c->tau.p;
     C.tauc = c->tauc.p;
@@ -932,6 +959,7 @@ int acs_gpu_get_counters(const acs_gpu_ctx *c, acs_counters *o) {
     o->fallback_full = h[kCntFallbackFull];
     o->relaxed_writes = h[kCntRelaxedWrites];
     o->lost_updates = h[kCntLost];
+    o->fallback_grid = h[kCntFallbackGrid];
     return ACS_OK;
 }
 

@@ -236,6 +236,83 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
                 return;
             }
         }
+        // Past the ext rows: rings of grid cells around cur, nearest first.
+        // Every node closer than the last ext entry is a candidate or an ext
+        // entry (scanned), so the walk starts at the first ring that can hold a
+        // farther node; before ring r every unscanned node is at Euclidean
+        // distance >= (r - 1) h, so its TSPLIB distance is >= floor((r - 1) h
+        // - 0.5) and its score <= tau_bound * eta^beta of that: once that bound
+        // is below the best, the result equals the full scan's (ties -> lowest id).
+        if (C.grid_g && C.ext_len) {
+            const int g = static_cast<int>(C.grid_g);
+            const double h = C.grid_h;
+            const int ccx = min(g - 1, static_cast<int>((xc - C.grid_x0) / h));
+            const int ccy = min(g - 1, static_cast<int>((yc - C.grid_y0) / h));
+            const double dext = static_cast<double>(__shfl_sync(kFull, q.y, 31));
+            int r = max(0, static_cast<int>(ceil((dext - 0.5) / (h * 1.4142135623730951))) - 1);
+            for (;; ++r) {
+                double sb = bs;
+                uint32_t node = have ? bv : 0xffffffffu;
+                warp_argmax_node(sb, node, have);
+                const double dlo = r >= 1 ? (r - 1) * h - 0.5 : 0.0;
+                const int32_t dl = max(1, static_cast<int32_t>(floor(dlo)));
+                const double bound = __dmul_rn(C.tau_bound, eta_beta_i(I, dl, C.beta, C.beta_int));
+                const bool outside = r > g;  // every cell scanned
+                if (node != 0xffffffffu && (outside || bound < sb)) {
+                    const unsigned owner = __ballot_sync(kFull, have && bv == node);
+                    const int src = __ffs(owner) - 1;
+                    finish_scan(I, C, cur, node, __shfl_sync(kFull, bt, src), lane, o);
+                    if (lane == 0) atomicAdd(C.counters + kCntFallbackGrid, 1ull);
+                    return;
+                }
+                if (outside) break;  // no unvisited node at all: not reachable in a fallback
+                // ring r: 8r cells (1 for r = 0), 32 at a time one per lane; their
+                // nodes enumerated 32 per round in lockstep (tau_of may shuffle)
+                const int ncell = r ? 8 * r : 1;
+                for (int c0 = 0; c0 < ncell; c0 += 32) {
+                    const int k = c0 + lane;
+                    int cx = ccx, cy = ccy;
+                    if (r) {
+                        const int side = 2 * r + 1;
+                        if (k < side) { cx = ccx - r + k; cy = ccy - r; }
+                        else if (k < 2 * side) { cx = ccx - r + (k - side); cy = ccy + r; }
+                        else if (k < 2 * side + (side - 2)) { cx = ccx - r; cy = ccy - r + 1 + (k - 2 * side); }
+                        else { cx = ccx + r; cy = ccy - r + 1 + (k - 2 * side - (side - 2)); }
+                    }
+                    const bool inside = k < ncell && cx >= 0 && cy >= 0 && cx < g && cy < g;
+                    const uint32_t cell = inside ? static_cast<uint32_t>(cy) * C.grid_g + static_cast<uint32_t>(cx) : 0u;
+                    const uint32_t cs = inside ? __ldg(C.cell_start + cell) : 0u;
+                    const uint32_t cnt = inside ? __ldg(C.cell_start + cell + 1) - cs : 0u;
+                    uint32_t incl = cnt;
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const uint32_t t = __shfl_up_sync(kFull, incl, off);
+                        if (lane >= off) incl += t;
+                    }
+                    const uint32_t total = __shfl_sync(kFull, incl, 31);
+                    const uint32_t excl = incl - cnt;
+                    for (uint32_t b0 = 0; b0 < total; b0 += 32) {
+                        const uint32_t idx = b0 + lane;
+                        int src = 0;  // the last lane whose exclusive offset is <= idx owns it
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1)
+                            if (__shfl_sync(kFull, excl, src + step) <= idx) src += step;
+                        const uint32_t sc = __shfl_sync(kFull, cs, src);
+                        const uint32_t ex = __shfl_sync(kFull, excl, src);
+                        const uint32_t x = idx < total ? __ldg(C.cell_nodes + sc + (idx - ex)) : 0u;
+                        const bool act = idx < total && !visited(vis, x);
+                        const double tv = tau_of(x, act);  // every lane calls
+                        if (act) {
+                            const int32_t d = tsplib_distance(I.type, xc, yc, __ldg(I.xs + x), __ldg(I.ys + x));
+                            const double scv = __dmul_rn(tv, eta_beta_i(I, d, C.beta, C.beta_int));
+                            if (!have || scv > bs || (scv == bs && x < bv)) {
+                                have = true; bs = scv; bv = x; bt = tv; bm = kMirrorUnknown;
+                            }
+                        }
+                    }
+                }
+            }
+        }
     }
     if (lane == 0) atomicAdd(C.counters + kCntFallbackFull, 1ull);
     if constexpr (kDefer) {
@@ -752,6 +829,9 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             const bool mw = c == mprev;
             const size_t mi = static_cast<size_t>(cur) * 32 + lane;
             const double mval = kAtomic ? 0.0 : affine(tl, C.c_l, C.c_0);
+#ifdef ACS_COUNT_LOST
+            const double told = tl;  // the value this lane's update read (tl is reloaded below)
+#endif
             const int32_t dl = static_cast<int32_t>(el.y);
             int pos;
             uint32_t v;
@@ -820,13 +900,15 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
                 red_add_if(me, C.cnt + d_vu, one);
             } else {
 #ifdef ACS_COUNT_LOST
-                // instrumented build: every write is an exchange, and a write whose
-                // old value is not the one this update read lost another ant's update
+                // instrumented build: the candidate-copy write (the copy this lane
+                // read as tl) is an exchange; an old value other than tl means
+                // another ant's update of that trail landed in between and is lost
                 if (me || mw) {
-                    wc.writes += me ? 3 : 1;
-                    wc.lost += xchg_lost(C.tauc + mi, mval, tl);
-                    if (me) wc.lost += xchg_lost(C.tau + d_uv, mval, tl) + xchg_lost(C.tau + d_vu, mval, tl);
+                    ++wc.writes;
+                    wc.lost += xchg_lost(C.tauc + mi, mval, told);
                 }
+                st_relaxed_if(me, C.tau + d_uv, mval);
+                st_relaxed_if(me, C.tau + d_vu, mval);
 #else
                 st_relaxed_if(me || mw, C.tauc + mi, mval);
                 st_relaxed_if(me, C.tau + d_uv, mval);
@@ -1297,7 +1379,9 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
             prev = cur;
             const bool me = lane == pos;
             sts_if(me, vw, word | bit);
+#ifndef ACS_X_LEN_PASS
             lenl += me ? dl : 0;
+#endif
             if (greedy && cand) rng.advance();
             la.prepare(rng);
             route_put(route, rbuf, t, v, lane);
@@ -1321,7 +1405,9 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
         r2.load(rec8(C, start), lane);
         wc.misses += !spm8_update<true>(C, rec8(C, start), cur, 0.0, r2.idl, r2.val, r2.tail, lane);
         wc.hits = 2 * n - wc.misses;  // n local updates (k = 1), two record operations each
+#ifndef ACS_X_LEN_PASS
         if (lane == 0) C.lens[a] = len + dclose;
+#endif
         wc.flush(C.counters, lane, n - 1);
         __syncwarp();
     }
@@ -1599,293 +1685,6 @@ __global__ void __maxnreg__(kMaxRegs) k_deferred(DevInstance I, DevColony C, Dev
     if (close_due) {
         grid_sync();
         for (uint32_t j = 0; j < my_ants; ++j) fold_copy(C, n, ants[j].cur, ants[j].start, ants[j].slots, lane);
-    }
-    wc.flush(C.counters, lane, my_ants * (n - 1));
-}
-
-// ---- deferred, one grid barrier per step ----------------------------------
-//
-// Every copy of a trail has a 64-bit pending cell next to its base:
-//   bits  0-31  acc: updates of earlier steps not yet folded into the base
-//   bits 32-47  s0 / bits 48-63 s1: the updates of the last two steps, by parity
-// Step t bumps s[t & 1] of its edge's copies and moves its step t-1 bumps from
-// s[(t-1) & 1] into acc (one non-returning add: acc + 1, s - 1).  A reader at
-// step t takes c = acc + s[(t-1) & 1] -- invariant under the concurrent
-// moves, blind to the concurrent step-t bumps -- and applies f c times to the
-// base, in sequence: the value SYNC's ordered updates give (f^a then f^b is
-// f^(a+b), application by application).  So one barrier per step separates
-// the step's bumps from the next step's reads.  Every kDefFold steps (and at
-// the end of the iteration) a fold phase between two barriers moves acc into
-// the base: each ant folds the copies of its last kDefFold edges, and the
-// atomic swap of acc hands every copy's count to exactly one of them.
-constexpr uint32_t kDefFold = 8;              // fold period (steps)
-constexpr uint32_t kDefRing = kDefFold + 1;   // edges an ant remembers for its folds
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const unsigned long long *p) {
-    uint64_t r;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
-    return r;
-}
-__device__ __forceinline__ void red_add_u64(unsigned long long *p, unsigned long long v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-// f applied c times (SYNC's ordered local updates, P7)
-__device__ __forceinline__ double apply_f(double x, uint32_t c, const DevColony &C) {
-    for (uint32_t i = 0; i < c; ++i) x = affine(x, C.c_l, C.c_0);
-    return x;
-}
-// trail value a step-t reader sees: f^(acc + s[(t-1)&1])(base)
-__device__ __forceinline__ double def_trail(double base, uint64_t w, uint32_t t, const DevColony &C) {
-    const uint32_t c = static_cast<uint32_t>(w) + static_cast<uint32_t>((w >> (32 + 16 * ((t - 1) & 1))) & 0xFFFFu);
-    return apply_f(base, c, C);
-}
-
-struct DefSmem2 {
-    size_t ants_off, vis_off, ring_off, part_off, req_off, bytes;
-    __host__ __device__ DefSmem2(uint32_t wpb, uint32_t A, uint32_t words) {
-        ants_off = static_cast<size_t>(wpb) * 32 * sizeof(double);  // roulette scratch
-        vis_off = ants_off + static_cast<size_t>(wpb) * A * 64;      // DefAnt <= 64 B
-        ring_off = vis_off + static_cast<size_t>(wpb) * A * words * sizeof(uint32_t);
-        ring_off = (ring_off + 15) & ~static_cast<size_t>(15);
-        part_off = ring_off + static_cast<size_t>(wpb) * A * kDefRing * sizeof(uint4);
-        req_off = part_off + static_cast<size_t>(wpb) * A * wpb * sizeof(ScanPart);
-        bytes = req_off + (static_cast<size_t>(wpb) * A + 1) * sizeof(uint32_t);
-    }
-};
-
-// the pending cell of copy `lane` (0 tau[u][v], 1 tau[v][u], 2 tauc[u][pos],
-// 3 tauc[v][mirror]) of edge (u, v), nullptr when absent
-__device__ __forceinline__ unsigned long long *def_cell(const DevColony &C, const DevDeferred &D, uint32_t n,
-                                                        uint32_t u, uint32_t v, uint32_t slots, int lane,
-                                                        double **base) {
-    bool dense;
-    size_t k;
-    const int pos = (slots & 0xFFu) == 0xFFu ? -1 : static_cast<int>(slots & 0xFFu);
-    if (!copy_index(n, u, v, pos, (slots >> 8) & 0xFFu, lane, dense, k)) return nullptr;
-    *base = (dense ? C.tau : C.tauc) + k;
-    return (dense ? D.cell : D.cellc) + k;
-}
-
-template <class RNG>
-__global__ void __maxnreg__(kMaxRegs) k_deferred2(DevInstance I, DevColony C, DevDeferred D) {
-    static_assert(sizeof(DefAnt<RNG>) <= 64, "DefSmem2 reserves 64 B per ant");
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int wpb = blockDim.x >> 5;
-    const uint32_t A = D.ants_per_warp;
-    const uint32_t W = gridDim.x * wpb;
-    const uint32_t gw = wib * gridDim.x + blockIdx.x;
-    const uint32_t n = I.n;
-    const DefSmem2 L(wpb, A, I.words);
-    double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
-    DefAnt<RNG> *ants_cta = reinterpret_cast<DefAnt<RNG> *>(smem + L.ants_off);
-    DefAnt<RNG> *ants = ants_cta + wib * A;
-    uint32_t *vis_cta = reinterpret_cast<uint32_t *>(smem + L.vis_off);
-    uint32_t *vis_base = vis_cta + static_cast<size_t>(wib) * A * I.words;
-    uint4 *ring = reinterpret_cast<uint4 *>(smem + L.ring_off) + static_cast<size_t>(wib) * A * kDefRing;
-    ScanPart *parts = reinterpret_cast<ScanPart *>(smem + L.part_off);
-    uint32_t *nreq = reinterpret_cast<uint32_t *>(smem + L.req_off);
-    uint32_t *reqs = nreq + 1;
-    const uint32_t slice = ((I.words + wpb - 1) / wpb + 3) & ~3u;
-    const uint64_t it = *C.iter;
-    WarpCounters wc;
-    uint32_t my_ants = 0;
-    if (threadIdx.x == 0) *nreq = 0;
-
-    for (uint32_t j = 0; j < A; ++j) {
-        const uint32_t a = gw + j * W;
-        if (a >= C.m) break;
-        ++my_ants;
-        uint32_t *vis = vis_base + j * I.words;
-        for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
-        if (lane < static_cast<int>(kDefRing)) ring[j * kDefRing + lane] = make_uint4(0u, 0u, 0u, 0u);  // u = v: no edge
-        RNG rng;
-        rng_init(rng, C, it, a);
-        const uint32_t start = static_cast<uint32_t>(uniform_int(rng, n));
-        __syncwarp();
-        if (lane == 0) {
-            vis[start >> 5] |= 1u << (start & 31);
-            ants[j].rng = rng;
-            ants[j].len = 0;
-            ants[j].cur = start;
-            ants[j].start = start;
-            C.routes[static_cast<size_t>(a) * n] = start;
-        }
-        __syncwarp();
-    }
-    grid_sync();
-
-    // an ant's copies of one remembered edge: fold acc (phase) or everything (end)
-    auto fold_edge = [&](const uint4 &e, bool all) {
-        if (e.x == e.y) return;  // empty slot
-        double *bp;
-        unsigned long long *cp = def_cell(C, D, n, e.x, e.y, e.z, lane, &bp);
-        if (!cp) return;
-        const double x = ld_relaxed(bp);
-        const uint64_t w = all ? atomicExch(cp, 0ull) : atomicAnd(cp, 0xFFFFFFFF00000000ull);
-        const uint32_t c = all ? static_cast<uint32_t>(w) + static_cast<uint32_t>((w >> 32) & 0xFFFFu) +
-                                     static_cast<uint32_t>(w >> 48)
-                               : static_cast<uint32_t>(w);
-        if (c) st_relaxed(bp, apply_f(x, c, C));
-    };
-
-    for (uint32_t t = 1; t < n; ++t) {
-        // (1) selection against the step-start pheromone; undecided fallbacks post a request
-        for (uint32_t j = 0; j < my_ants; ++j) {
-            uint32_t *vis = vis_base + j * I.words;
-            DefAnt<RNG> &s = ants[j];
-            const uint32_t cur = s.cur;
-            RNG rng = s.rng;
-            const size_t ri = static_cast<size_t>(cur) * 32 + lane;
-            const uint4 el = __ldg(C.rows + ri);
-            const double tau_lane = def_trail(ld_relaxed(C.tauc + ri), ld_relaxed_u64(D.cellc + ri), t, C);
-            Lookahead<RNG> la;
-            la.prepare(rng);
-            Step st;
-            select_step<true>(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
-                              [&](uint32_t v, bool act) {
-                                  if (!act) return 0.0;
-                                  const size_t k = static_cast<size_t>(cur) * n + v;
-                                  return def_trail(ld_relaxed(C.tau + k), ld_relaxed_u64(D.cell + k), t, C);
-                              },
-                              st);
-            if (st.kind == 0) rng.advance();
-            __syncwarp();
-            if (lane == 0) {
-                s.rng = rng;
-                s.kind = st.kind;
-                if (st.kind == 3) {
-                    reqs[atomicAdd(nreq, 1u)] = (static_cast<uint32_t>(wib) << 16) | j;
-                } else {
-                    s.v = st.v;
-                    s.d = st.d;
-                    s.slots = (static_cast<uint32_t>(st.pos) & 0xFFu) | (st.mirror << 8);
-                }
-            }
-            __syncwarp();
-        }
-        // (2) the CTA's full scans, every warp one slice of each
-        __syncthreads();
-        const uint32_t nr = *nreq;
-        if (nr) {  // CTA-uniform
-            for (uint32_t r = 0; r < nr; ++r) {
-                const uint32_t q = reqs[r];
-                const uint32_t ow = q >> 16, oj = q & 0xFFFFu;
-                const uint32_t *vis = vis_cta + (static_cast<size_t>(ow) * A + oj) * I.words;
-                const uint32_t cur = ants_cta[ow * A + oj].cur;
-                const uint32_t wb = wib * slice, we = min(wb + slice, I.words);
-                ScanBest b;
-                if (wb < we)
-                    full_scan_range(I, C, vis, cur,
-                                    [&](uint32_t v, bool act) {
-                                        if (!act) return 0.0;
-                                        const size_t k = static_cast<size_t>(cur) * n + v;
-                                        return def_trail(ld_relaxed(C.tau + k), ld_relaxed_u64(D.cell + k), t, C);
-                                    },
-                                    lane, wb, we, b);
-                double sc = b.bs;
-                uint32_t node = b.have ? b.bv : 0xffffffffu;
-                warp_argmax_node(sc, node, b.have);
-                const unsigned owner = __ballot_sync(kFull, b.have && b.bv == node);
-                const double tv = __shfl_sync(kFull, b.bt, owner ? __ffs(owner) - 1 : 0);
-                if (lane == 0) parts[r * wpb + wib] = ScanPart{sc, tv, node};
-            }
-            __syncthreads();
-            for (uint32_t r = 0; r < nr; ++r) {
-                const uint32_t q = reqs[r];
-                if ((q >> 16) != static_cast<uint32_t>(wib)) continue;  // warp-uniform
-                DefAnt<RNG> &s = ants[q & 0xFFFFu];
-                const bool ok = lane < wpb && parts[r * wpb + lane].v != 0xffffffffu;
-                const ScanPart pp = ok ? parts[r * wpb + lane] : ScanPart{0.0, 0.0, 0xffffffffu};
-                double sc = pp.s;
-                uint32_t node = pp.v;
-                warp_argmax_node(sc, node, ok);
-                const unsigned owner = __ballot_sync(kFull, ok && pp.v == node);
-                Step st;
-                finish_scan(I, C, s.cur, node, __shfl_sync(kFull, pp.t, __ffs(owner) - 1), lane, st);
-                __syncwarp();
-                if (lane == 0) {
-                    s.kind = 2;
-                    s.v = st.v;
-                    s.d = st.d;
-                    s.slots = 0xFFu | (st.mirror << 8);
-                }
-                __syncwarp();
-            }
-            __syncthreads();  // every warp has read *nreq and its parts
-            if (threadIdx.x == 0) *nreq = 0;
-        }
-        // (3) bump this step's copies (s[t&1]), move last step's into acc, remember the edge
-        const bool due = (t % C.k) == 0;
-        for (uint32_t j = 0; j < my_ants; ++j) {
-            const uint32_t a = gw + j * W;
-            uint32_t *vis = vis_base + j * I.words;
-            DefAnt<RNG> &s = ants[j];
-            const uint32_t v = s.v, slots = s.slots;
-            wc.count(s.kind, n - t);
-            double *bp;
-            if (due) {
-                ++wc.updates;
-                unsigned long long *cp = def_cell(C, D, n, s.cur, v, slots, lane, &bp);
-                if (cp) red_add_u64(cp, 1ull << (32 + 16 * (t & 1)));
-            }
-            // the previous step's edge (its ring entry) -- moved from s[(t-1)&1] into acc
-            const uint4 pe = ring[j * kDefRing + (t - 1) % kDefRing];
-            if (t >= 2 && pe.w) {
-                unsigned long long *cp = def_cell(C, D, n, pe.x, pe.y, pe.z, lane, &bp);
-                if (cp) red_add_u64(cp, 1ull - (1ull << (32 + 16 * ((t - 1) & 1))));
-            }
-            __syncwarp();
-            if (lane == 0) {
-                ring[j * kDefRing + t % kDefRing] = make_uint4(s.cur, v, slots, due ? 1u : 0u);
-                vis[v >> 5] |= 1u << (v & 31);
-                C.routes[static_cast<size_t>(a) * n + t] = v;
-                s.len += s.d;
-                s.cur = v;
-            }
-            __syncwarp();
-        }
-        grid_sync();
-        // (4) every kDefFold steps: fold acc of the last kDefFold edges into the bases
-        if (t % kDefFold == 0) {
-            for (uint32_t j = 0; j < my_ants; ++j)
-                for (uint32_t r = 0; r < kDefRing; ++r) fold_edge(ring[j * kDefRing + r], false);
-            grid_sync();
-        }
-    }
-
-    // closing edges (edge n of every ant): bump s[n&1], move step n-1's
-    const bool close_due = (n % C.k) == 0;
-    for (uint32_t j = 0; j < my_ants; ++j) {
-        const uint32_t a = gw + j * W;
-        DefAnt<RNG> &s = ants[j];
-        int pos;
-        uint32_t mirror;
-        int32_t d;
-        bool have_d;
-        closing_slots(C, s.cur, s.start, lane, pos, mirror, d, have_d);
-        if (!have_d)
-            d = tsplib_distance(I.type, __ldg(I.xs + s.cur), __ldg(I.ys + s.cur), __ldg(I.xs + s.start),
-                                __ldg(I.ys + s.start));
-        const uint32_t slots = (static_cast<uint32_t>(pos) & 0xFFu) | (mirror << 8);
-        double *bp;
-        if (close_due) {
-            ++wc.updates;
-            unsigned long long *cp = def_cell(C, D, n, s.cur, s.start, slots, lane, &bp);
-            if (cp) red_add_u64(cp, 1ull << (32 + 16 * (n & 1)));
-        }
-        __syncwarp();
-        if (lane == 0) {
-            C.lens[a] = s.len + d;
-            s.slots = slots;  // the closing edge (cur, start), folded below
-        }
-        __syncwarp();
-    }
-    grid_sync();
-    // final fold: every pending count (acc and both slots) of the last
-    // kDefRing edges -- all steps since the last fold phase -- and the closing edge
-    for (uint32_t j = 0; j < my_ants; ++j) {
-        for (uint32_t r = 0; r < kDefRing; ++r) fold_edge(ring[j * kDefRing + r], true);
-        fold_edge(make_uint4(ants[j].cur, ants[j].start, ants[j].slots, 1u), true);
     }
     wc.flush(C.counters, lane, my_ants * (n - 1));
 }
@@ -2389,6 +2188,9 @@ static void launch_spm_rng(const DevInstance &I, const DevColony &C, bool one_wa
                 launch_tour_kernel(k_construct_spm<8, RNG, true>, I, C, false, s);
 #else
                 launch_tour_kernel(k_spm_lean<RNG>, I, C, false, s);
+#ifdef ACS_X_LEN_PASS
+                launch_tour_lengths(I, C.routes, C.m, C.lens, s);
+#endif
 #endif
             }
             else launch_tour_kernel(k_construct_spm<8, RNG>, I, C, one_warp, s);
@@ -2428,13 +2230,8 @@ static int deferred_launch(const DevInstance &I, const DevColony &C, DevDeferred
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int wpb = kDefBlock / 32;
-#ifndef ACS_X_NEW_DEFERRED
     auto kern = k_deferred<RNG>;
     auto smem_of = [&](uint32_t a) { return DefSmem(wpb, a, I.words).bytes; };
-#else
-    auto kern = k_deferred2<RNG>;
-    auto smem_of = [&](uint32_t a) { return DefSmem2(wpb, a, I.words).bytes; };
-#endif
     uint32_t A = 1;
     size_t smem = 0;
     for (;; ++A) {

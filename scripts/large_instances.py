@@ -50,11 +50,13 @@ def main():
                        "device_bytes": int(info.device_bytes),
                        "fallback_steps_per_iter": round((c1["fallback_steps"] - c0["fallback_steps"]) / it, 1),
                        "fallback_full_per_iter": round((c1["fallback_full"] - c0["fallback_full"]) / it, 1),
+                       "fallback_grid_per_iter": round((c1["fallback_grid"] - c0["fallback_grid"]) / it, 1),
                        "steps_per_iter": col.m * (n - 1), "best_len_after": int(best)}
                 rec["fallback_full_share"] = round(rec["fallback_full_per_iter"] / max(rec["fallback_steps_per_iter"], 1), 4)
                 res["results"][f"rnd{n}/m{col.m}/{v}"] = rec
                 print(json.dumps({k: rec[k] for k in ("n", "m", "construct_ms", "tours_per_s", "device_bytes",
-                                                      "fallback_steps_per_iter", "fallback_full_per_iter")}),
+                                                      "fallback_steps_per_iter", "fallback_full_per_iter",
+                                                      "fallback_grid_per_iter")}),
                       v, flush=True)
     if a.out:
         json.dump(res, open(a.out, "w"), indent=1)

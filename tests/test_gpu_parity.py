@@ -280,15 +280,21 @@ def test_colony_larger_than_one_wave(acs, orc, gpu, variant):
     assert st["iter_best_len"].tolist()[-1] == lens.min()
 
 
+@pytest.mark.parametrize("grid", [True, False])
 @pytest.mark.parametrize("mode", ["sync", "seq"])
-def test_no_eta_table_bit_exact(acs, orc, gpu, mode):
-    """n > 4096: no eta^beta table, so every undecided fallback runs the
-    compacted scan (deferred: split over the warps of the CTA).  q0 = 0.5 and
-    few ants keep fallbacks frequent and late, where the pruned pass gives up."""
+def test_no_eta_table_bit_exact(acs, orc, gpu, monkeypatch, mode, grid):
+    """n > 4096: no eta^beta table.  A fallback the ext rows cannot settle
+    walks rings of grid cells (grid) or runs the compacted scan over the
+    unvisited nodes (ACS_NO_GRID; deferred: split over the warps of the CTA).
+    q0 = 0.5 and few ants keep fallbacks frequent and late."""
+    if grid:
+        monkeypatch.delenv("ACS_NO_GRID", raising=False)
+    else:
+        monkeypatch.setenv("ACS_NO_GRID", "1")
     I = small_instance(4200, seed=3, scale=20000)
     r = pair(acs, orc, I, mode, O.DENSE, m=48 if mode == "sync" else 6, iters=2, seed=2, q0=0.5, k=2)
     check_exact(*r, O.DENSE)
-    assert r[4]["fallback_full"] > 0
+    assert (r[4]["fallback_grid"] if grid else r[4]["fallback_full"]) > 0
 
 
 def test_sync_cooperative_scan_bit_exact(acs, orc, gpu):

@@ -19,6 +19,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from helpers import to_acs
 from test_gpu_parity import check_exact, pair
 
 pytestmark = pytest.mark.gpu
@@ -65,4 +66,34 @@ def test_rnd10k_bit_exact(acs, orc, gpu, mode, memory):
     I = O.rnd_instance(10000)
     r = pair(acs, orc, I, mode, memory, m=64, iters=1, seed=8)
     check_exact(*r, memory)
-    assert r[4]["fallback_full"] > 0  # the compacted full scan was exercised
+    # fallbacks past the ext rows: settled by the grid rings (or the compacted full scan)
+    assert r[4]["fallback_grid"] + r[4]["fallback_full"] > 0
+
+
+@pytest.mark.parametrize("variant", ["seq", "deferred"])
+def test_rnd10k_grid_ring_fallback_equals_full_scan(acs, orc, gpu, monkeypatch, variant):
+    """n > 4096: a fallback the ext rows cannot settle walks rings of grid
+    cells before giving up to the full scan.  The grid walk must give the
+    full scan's answer: the same tours and pheromone with and without it
+    (ACS_NO_GRID), and the oracle's."""
+    I = O.rnd_instance(10000)
+    out = {}
+    for grid in (True, False):
+        if grid:
+            monkeypatch.delenv("ACS_NO_GRID", raising=False)
+        else:
+            monkeypatch.setenv("ACS_NO_GRID", "1")
+        p = acs.AcsParams(variant=variant, m=16, seed=4, q0=0.6)
+        with acs.Colony(to_acs(acs, I), p) as col:
+            st = col.iterate(1)
+            routes, _ = col.routes()
+            tau = col.pheromone()
+            out[grid] = (st["global_best_len"].tolist(), routes, tau, col.counters())
+    g, f = out[True], out[False]
+    assert g[0] == f[0] and (g[1] == f[1]).all()
+    assert np.array_equal(g[2].view(np.uint64), f[2].view(np.uint64))
+    assert g[3]["fallback_grid"] > 0 and f[3]["fallback_grid"] == 0
+    assert g[3]["fallback_full"] < f[3]["fallback_full"]
+    o = orc.run(I, m=16, iterations=1, seed=4, mode=O.SYNC if variant == "deferred" else O.SEQ, q0=0.6,
+                want_routes=True)
+    assert (g[1] == o["routes"]).all()
