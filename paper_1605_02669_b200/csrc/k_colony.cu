@@ -893,12 +893,15 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             // prev writes the late mirror copy of the previous edge; the fourth
             // copy, tauc[v][mirror], is next step's late copy.
             const bool me = lane == pos;
-            const size_t d_uv = static_cast<size_t>(cur) * n + v, d_vu = static_cast<size_t>(v) * n + cur;
             if constexpr (kAtomic) {
                 red_add_if(me || mw, C.cntc + mi, one);
-                red_add_if(me, C.cnt + d_uv, one);
-                red_add_if(me, C.cnt + d_vu, one);
+                // the two dense counters in one instruction: lane pos bumps
+                // cnt[u][v], lane pos ^ 1 bumps cnt[v][u] (no value to move)
+                const bool mate = lane == (pos ^ 1);
+                const uint32_t row = me ? cur : v;
+                red_add_if(pos >= 0 && (me || mate), C.cnt + (static_cast<size_t>(row) * n + (cur ^ v ^ row)), one);
             } else {
+                const size_t d_uv = static_cast<size_t>(cur) * n + v, d_vu = static_cast<size_t>(v) * n + cur;
 #ifdef ACS_COUNT_LOST
                 // instrumented build: the candidate-copy write (the copy this lane
                 // read as tl) is an exchange; an old value other than tl means
