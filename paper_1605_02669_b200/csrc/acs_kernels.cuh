@@ -127,7 +127,7 @@ void launch_topk(const DevInstance &I, uint32_t L, uint32_t *out, cudaStream_t s
 void launch_build_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, double beta,
                        int beta_int, uint4 *rows, cudaStream_t s);
 void launch_nn_tour_cand(const DevInstance &I, const uint32_t *cand, uint32_t L, uint32_t start, int64_t *out,
-                         cudaStream_t s);
+                         cudaStream_t s, const uint4 *ext = nullptr, uint32_t ext_len = 0);
 void launch_tour_lengths(const DevInstance &I, const uint32_t *routes, uint32_t m, int64_t *out,
                          cudaStream_t s);
 void launch_eta_table(const DevInstance &I, double beta, int beta_int, double *out,

@@ -637,7 +637,8 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     }
     // tau0 = 1/(n * L_nn) from the NN tour from node 0
     CUDA_TRY(c->best_len.alloc(1));
-    launch_nn_tour_cand(I, c->cand.p, c->L, 0, c->best_len.p, s);
+    launch_nn_tour_cand(I, c->cand.p, c->L, 0, c->best_len.p, s, c->ext.p,
+                        c->ext.p ? static_cast<uint32_t>(c->ext.count / n) : 0u);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(&c->nn_len, c->best_len.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));

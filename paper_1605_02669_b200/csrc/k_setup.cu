@@ -7,6 +7,7 @@
 //   K6 k_tour_lengths     tsp_instance.cpp:67-78 tour_length (validation / eval)
 //   plus device RNG and selective-store op scripts used by the parity tests.
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 
 #include "../../include/acs_gpu.h"
@@ -166,7 +167,8 @@ __global__ void k_build_rows(DevInstance I, const uint32_t *cand, uint32_t L, do
 // visited does the warp scan all n nodes.  ~2% of steps scan, so the setup
 // drops from n block-wide scans to n list probes.
 __global__ void __launch_bounds__(32) k_nn_tour_cand(DevInstance I, const uint32_t *cand, uint32_t L,
-                                                     uint32_t start, int64_t *out) {
+                                                     uint32_t start, int64_t *out, const uint4 *ext,
+                                                     uint32_t ext_len) {
     extern __shared__ uint32_t vis[];
     const int lane = threadIdx.x & 31;
     for (uint32_t i = lane; i < I.words; i += 32) vis[i] = 0;
@@ -182,10 +184,28 @@ __global__ void __launch_bounds__(32) k_nn_tour_cand(DevInstance I, const uint32
         const unsigned um = __ballot_sync(kFull, in && !visited(vis, c));
         uint32_t next;
         int32_t d;
-        if (um) {
+        bool found = um != 0u;
+        if (found) {
             next = __shfl_sync(kFull, c, __ffs(um) - 1);
             d = dist_of(I, cur, next, xc, yc);
-        } else {
+        }
+        // every candidate visited: the next-nearest rows (sorted by (d, id),
+        // like the full scan's key) hold the answer when any of them is unvisited
+        for (uint32_t base = 0; !found && base < ext_len; base += 32) {
+            const uint4 q = __ldg(ext + static_cast<size_t>(cur) * ext_len + base + lane);
+            const bool ok = q.x != kEmpty;
+            const uint32_t id = q.x & kIdMask;
+            const unsigned ue = __ballot_sync(kFull, ok && !visited(vis, id));
+            if (ue) {
+                const int src = __ffs(ue) - 1;
+                next = __shfl_sync(kFull, id, src);
+                d = static_cast<int32_t>(__shfl_sync(kFull, q.y, src));
+                found = true;
+            } else if (__any_sync(kFull, !ok)) {
+                break;  // the list ended
+            }
+        }
+        if (!found) {
             uint64_t best = ~0ull;
             for (uint32_t v = lane; v < I.n; v += 32) {
                 if (visited(vis, v)) continue;
@@ -208,6 +228,95 @@ __global__ void __launch_bounds__(32) k_nn_tour_cand(DevInstance I, const uint32
         cur = next;
     }
     if (lane == 0) *out = total + dist_of(I, cur, start, __ldg(I.xs + cur), __ldg(I.ys + cur));
+}
+
+// The same NN tour with the candidate lists staged in shared memory as 16-bit
+// ids (n < 65536, n*L*2 B within the CTA's shared memory): the walk's
+// dependent load per step is then an LDS instead of an L2 round trip.  The
+// route is kept in shared memory and the length summed afterwards by the
+// whole CTA, so no distance load sits in the walk either.  Same answer as
+// k_nn_tour_cand (candidates first, then the next-nearest rows, then the full
+// scan; ties -> lowest id).
+__global__ void __launch_bounds__(1024) k_nn_tour_smem(DevInstance I, const uint32_t *cand, uint32_t L,
+                                                      uint32_t start, int64_t *out, const uint4 *ext,
+                                                      uint32_t ext_len) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t n = I.n;
+    uint32_t *vis = reinterpret_cast<uint32_t *>(smem);
+    uint32_t *route = vis + I.words;
+    uint16_t *c16 = reinterpret_cast<uint16_t *>(route + n);
+    __shared__ long long part[32];
+    for (uint32_t i = threadIdx.x; i < I.words; i += blockDim.x) vis[i] = 0;
+    for (size_t i = threadIdx.x; i < static_cast<size_t>(n) * L; i += blockDim.x) c16[i] = static_cast<uint16_t>(cand[i]);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        if (lane == 0) {
+            vis[start >> 5] |= 1u << (start & 31);
+            route[0] = start;
+        }
+        __syncwarp();
+        uint32_t cur = start;
+        for (uint32_t step = 1; step < n; ++step) {
+            const bool in = static_cast<uint32_t>(lane) < L;
+            const uint32_t c = in ? c16[static_cast<size_t>(cur) * L + lane] : 0u;
+            const unsigned um = __ballot_sync(kFull, in && !visited(vis, c));
+            uint32_t next = 0;
+            bool found = um != 0u;
+            if (found) next = __shfl_sync(kFull, c, __ffs(um) - 1);
+            for (uint32_t base = 0; !found && base < ext_len; base += 32) {
+                const uint4 q = __ldg(ext + static_cast<size_t>(cur) * ext_len + base + lane);
+                const bool ok = q.x != kEmpty;
+                const uint32_t id = q.x & kIdMask;
+                const unsigned ue = __ballot_sync(kFull, ok && !visited(vis, id));
+                if (ue) {
+                    next = __shfl_sync(kFull, id, __ffs(ue) - 1);
+                    found = true;
+                } else if (__any_sync(kFull, !ok)) {
+                    break;
+                }
+            }
+            if (!found) {
+                const double xc = __ldg(I.xs + cur), yc = __ldg(I.ys + cur);
+                uint64_t best = ~0ull;
+                for (uint32_t v = lane; v < n; v += 32) {
+                    if (visited(vis, v)) continue;
+                    const int32_t dv = dist_of(I, cur, v, xc, yc);
+                    const uint64_t key = (static_cast<uint64_t>(static_cast<uint32_t>(dv)) << 32) | v;
+                    best = key < best ? key : best;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const uint64_t p = shfl_xor_u64(best, o);
+                    best = p < best ? p : best;
+                }
+                next = static_cast<uint32_t>(best);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                vis[next >> 5] |= 1u << (next & 31);
+                route[step] = next;
+            }
+            __syncwarp();
+            cur = next;
+        }
+    }
+    __syncthreads();
+    // closed-tour length, every thread a share of the edges
+    long long acc = 0;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t u = route[i], v = route[i + 1 == n ? 0 : i + 1];
+        acc += dist_of(I, u, v, __ldg(I.xs + u), __ldg(I.ys + u));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += static_cast<long long>(shfl_xor_u64(static_cast<uint64_t>(acc), o));
+    if (lane == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) t += part[w];
+        *out = t;
+    }
 }
 
 // K6: warp per route, int64 closed-tour sum (cpp:67-78)
@@ -316,8 +425,16 @@ void launch_build_rows(const DevInstance &I, const uint32_t *cand, uint32_t L, d
 
 
 void launch_nn_tour_cand(const DevInstance &I, const uint32_t *cand, uint32_t L, uint32_t start, int64_t *out,
-                         cudaStream_t s) {
-    k_nn_tour_cand<<<1, 32, I.words * sizeof(uint32_t), s>>>(I, cand, L, start, out);
+                         cudaStream_t s, const uint4 *ext, uint32_t ext_len) {
+    const size_t smem = static_cast<size_t>(I.words) * 4 + static_cast<size_t>(I.n) * 4 +
+                        static_cast<size_t>(I.n) * L * sizeof(uint16_t);
+    if (I.n < 65536 && smem <= 200 * 1024 && !std::getenv("ACS_NN_GLOBAL")) {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_nn_tour_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k_nn_tour_smem<<<1, 1024, smem, s>>>(I, cand, L, start, out, ext, ext_len);
+        return;
+    }
+    k_nn_tour_cand<<<1, 32, I.words * sizeof(uint32_t), s>>>(I, cand, L, start, out, ext, ext_len);
 }
 
 void launch_tour_lengths(const DevInstance &I, const uint32_t *routes, uint32_t m, int64_t *out,
