@@ -84,6 +84,21 @@ __device__ __forceinline__ double spm_read_mem(const SpmMem &M, uint32_t u, uint
 }
 
 
+// SM count of the current device (grid sizing of the grid-stride kernels)
+static inline unsigned device_sms() {
+    static thread_local int cached_dev = -1;
+    static thread_local unsigned cached_sms = 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != cached_dev) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cached_dev = dev;
+        cached_sms = sms > 0 ? static_cast<unsigned>(sms) : 1u;
+    }
+    return cached_sms;
+}
+
 static inline unsigned blocks_for(size_t work, unsigned per) {
     return static_cast<unsigned>((work + per - 1) / per);
 }

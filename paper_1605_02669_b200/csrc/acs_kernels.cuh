@@ -115,6 +115,11 @@ struct DevSpmSync {
     void *ants;            // m x SyncAnt<RNG>
     uint32_t *vis;         // m x words
     uint4 *ops;            // 2m {key lo, key hi, neighbour, 0}
+    // colonies above one CTA's sort (m > 8192): device-wide radix sort of the keys
+    unsigned long long *keys_in, *keys_out;  // 2m
+    uint32_t *idx_in, *idx_out;              // 2m
+    void *sort_tmp;
+    size_t sort_tmp_bytes;
 };
 
 struct DevDeferred {
@@ -159,6 +164,7 @@ int launch_deferred(int rng, const DevInstance &I, const DevColony &C, const Dev
 // global update on the best tour, stats[slot], iter++
 int launch_spm_sync(int rng, const DevInstance &I, const DevColony &C, const DevSpmSync &Y, cudaStream_t s);
 size_t spm_sync_ant_bytes();
+size_t spm_sync_sort_tmp_bytes(uint32_t count);  // cub::DeviceRadixSort temp storage for 2m keys
 void launch_epilogue(bool spm, bool fold, const DevInstance &I, const DevColony &C,
                      const DevBest &B, uint32_t slot, cudaStream_t s);
 // island import: adopt (tour,len) from device buffers if strictly better

@@ -243,6 +243,9 @@ struct acs_gpu_ctx {
     DBuf<unsigned char> sy_ants;  // SYNC x SELECTIVE: per-ant state, bitmasks, step ops
     DBuf<uint32_t> sy_vis;
     DBuf<uint4> sy_ops;
+    DBuf<unsigned long long> sy_keys;  // m > 8192: radix-sort keys (in | out)
+    DBuf<uint32_t> sy_idx;             // and their op indices
+    DBuf<unsigned char> sy_tmp;        // cub temp storage
     DevSpmSync spm_sync{};
 
     ~acs_gpu_ctx() {
@@ -704,11 +707,25 @@ int acs_gpu_create(const acs_instance_desc *inst, const acs_params *p, int devic
     }
     if (p->variant == ACS_VARIANT_SPM_SYNC) {
         // the apply pass sorts the step's 2m ops in one CTA's shared memory
-        if (c->m > 8192) return fail(ACS_E_ARG, "spm-sync (SYNC x SELECTIVE parity mode) supports m <= 8192");
+        // above 8192 ants the step's record operations are sorted device-wide (cub)
         CUDA_TRY(c->sy_ants.alloc(static_cast<size_t>(c->m) * spm_sync_ant_bytes()));
         CUDA_TRY(c->sy_vis.alloc(static_cast<size_t>(c->m) * I.words));
         CUDA_TRY(c->sy_ops.alloc(static_cast<size_t>(c->m) * 2));
-        c->spm_sync = DevSpmSync{c->sy_ants.p, c->sy_vis.p, c->sy_ops.p};
+        c->spm_sync = DevSpmSync{c->sy_ants.p, c->sy_vis.p, c->sy_ops.p, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+        if (c->m > 8192 || std::getenv("ACS_SSYNC_WIDE")) {
+            const size_t count = static_cast<size_t>(c->m) * 2;
+            CUDA_TRY(c->sy_keys.alloc(2 * count));
+            CUDA_TRY(c->sy_idx.alloc(2 * count));
+            const size_t tmp = spm_sync_sort_tmp_bytes(static_cast<uint32_t>(count));
+            CUDA_TRY(c->sy_tmp.alloc(tmp));
+            DevSpmSync &Y = c->spm_sync;
+            Y.keys_in = c->sy_keys.p;
+            Y.keys_out = c->sy_keys.p + count;
+            Y.idx_in = c->sy_idx.p;
+            Y.idx_out = c->sy_idx.p + count;
+            Y.sort_tmp = c->sy_tmp.p;
+            Y.sort_tmp_bytes = tmp;
+        }
     }
 
     DevColony &C = c->colony;

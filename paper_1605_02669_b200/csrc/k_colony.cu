@@ -18,6 +18,7 @@
 #include <cstdlib>
 
 #include <cooperative_groups.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include "../../include/acs_gpu.h"
 #include "acs_common.cuh"
@@ -1864,6 +1865,59 @@ __global__ void __launch_bounds__(1024) k_ssync_apply(DevColony C, DevSpmSync Y,
     if (misses) atomicAdd(C.counters + kCntMisses, misses);
 }
 
+// Large colonies: the step's keys sorted device-wide (cub radix sort, stable,
+// 56 key bits: record < 2^24 above (ant << 1 | u/v)), then a thread per
+// record segment applies its operations in order -- the k_ssync_apply walk.
+__global__ void k_ssync_keys(DevSpmSync Y, uint32_t count) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint4 o = Y.ops[i];
+    Y.keys_in[i] = (static_cast<unsigned long long>(o.y) << 32) | o.x;
+    Y.idx_in[i] = i;
+}
+
+__global__ void k_ssync_apply_sorted(DevColony C, DevSpmSync Y, uint32_t count) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long hits = 0, misses = 0;
+    if (i < count) {
+        const unsigned long long k = Y.keys_out[i];
+        const uint32_t r = static_cast<uint32_t>(k >> 32);
+        const bool head = k != ~0ull && (i == 0 || static_cast<uint32_t>(Y.keys_out[i - 1] >> 32) != r);
+        if (head) {
+            for (uint32_t j = i; j < count && Y.keys_out[j] != ~0ull && static_cast<uint32_t>(Y.keys_out[j] >> 32) == r;
+                 ++j) {
+                const uint4 o = Y.ops[Y.idx_out[j]];
+                if (spm_update_mem(C.spm, r, o.z, C.c_l, C.c_0, C.tau_min, nullptr)) ++hits; else ++misses;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        hits += __shfl_xor_sync(kFull, hits, o);
+        misses += __shfl_xor_sync(kFull, misses, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (hits | misses)) {
+        atomicAdd(C.counters + kCntHits, hits);
+        atomicAdd(C.counters + kCntMisses, misses);
+    }
+}
+
+size_t spm_sync_sort_tmp_bytes(uint32_t count) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const unsigned long long *>(nullptr),
+                                    static_cast<unsigned long long *>(nullptr), static_cast<const uint32_t *>(nullptr),
+                                    static_cast<uint32_t *>(nullptr), static_cast<int>(count), 0, 56);
+    return bytes;
+}
+
+static void spm_sync_apply_wide(const DevColony &C, const DevSpmSync &Y, uint32_t count, cudaStream_t s) {
+    k_ssync_keys<<<blocks_for(count, 256), 256, 0, s>>>(Y, count);
+    size_t bytes = Y.sort_tmp_bytes;
+    cub::DeviceRadixSort::SortPairs(Y.sort_tmp, bytes, Y.keys_in, Y.keys_out, Y.idx_in, Y.idx_out,
+                                    static_cast<int>(count), 0, 56, s);
+    k_ssync_apply_sorted<<<blocks_for(count, 256), 256, 0, s>>>(C, Y, count);
+}
+
 template <class RNG>
 static int spm_sync_iteration(const DevInstance &I, const DevColony &C, const DevSpmSync &Y, cudaStream_t s) {
     const unsigned wpb = 4, grid = blocks_for(C.m, wpb);
@@ -1871,17 +1925,25 @@ static int spm_sync_iteration(const DevInstance &I, const DevColony &C, const De
     uint32_t pow2 = 1;
     while (pow2 < count) pow2 <<= 1;
     const size_t apply_smem = static_cast<size_t>(pow2) * (sizeof(uint64_t) + sizeof(uint32_t));
-    if (apply_smem > 200 * 1024) return -1;
-    cudaFuncSetAttribute(k_ssync_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(apply_smem));
+    // above one CTA's sort: device-wide radix sort (also when the context
+    // allocated it for a smaller colony: ACS_SSYNC_WIDE, the test of that path)
+    const bool wide = apply_smem > 200 * 1024 || Y.sort_tmp;
+    if (wide && !Y.sort_tmp) return -1;
+    if (!wide)
+        cudaFuncSetAttribute(k_ssync_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(apply_smem));
+    auto apply = [&] {
+        if (wide) spm_sync_apply_wide(C, Y, count, s);
+        else k_ssync_apply<<<1, 1024, apply_smem, s>>>(C, Y, count, pow2);
+    };
     k_ssync_init<RNG><<<grid, wpb * 32, 0, s>>>(I, C, Y);
     for (uint32_t t = 1; t < I.n; ++t) {
         const int due = (t % C.k) == 0;
         k_ssync_select<RNG><<<grid, wpb * 32, wpb * 32 * sizeof(double), s>>>(I, C, Y, t, due);
-        if (due) k_ssync_apply<<<1, 1024, apply_smem, s>>>(C, Y, count, pow2);
+        if (due) apply();
     }
     const int close_due = (I.n % C.k) == 0;
     k_ssync_close<RNG><<<grid, wpb * 32, 0, s>>>(I, C, Y, close_due);
-    if (close_due) k_ssync_apply<<<1, 1024, apply_smem, s>>>(C, Y, count, pow2);
+    if (close_due) apply();
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
@@ -2263,7 +2325,7 @@ void launch_epilogue(bool spm, bool fold, const DevInstance &I, const DevColony 
     k_best<<<1, 1024, 0, s>>>(C, B, I.n, slot);
     if (fold) {  // grid sized to the counters (4 per thread), at most 8 CTAs per SM
         const size_t dense = static_cast<size_t>(I.n) * I.n;
-        k_fold_counts<<<std::min<size_t>(148 * 8, blocks_for(dense / 4 + 1, 256)), 256, 0, s>>>(
+        k_fold_counts<<<std::min<size_t>(static_cast<size_t>(device_sms()) * 8, blocks_for(dense / 4 + 1, 256)), 256, 0, s>>>(
             C, dense, static_cast<size_t>(I.n) * 32);
     }
     if (spm) k_global_spm<<<blocks_for(I.n, 256), 256, 0, s>>>(I, C, B);

@@ -443,12 +443,12 @@ void launch_tour_lengths(const DevInstance &I, const uint32_t *routes, uint32_t 
 }
 
 void launch_fill(double *p, size_t count, double value, cudaStream_t s) {
-    k_fill<<<std::min<size_t>(blocks_for(count, 256), 148 * 16), 256, 0, s>>>(p, count, value);
+    k_fill<<<std::min<size_t>(blocks_for(count, 256), static_cast<size_t>(device_sms()) * 16), 256, 0, s>>>(p, count, value);
 }
 
 void launch_spm_init(const SpmMem &M, uint32_t n, double tau_min, cudaStream_t s) {
     const size_t work = static_cast<size_t>(n) * M.S;
-    k_spm_init<<<std::min<size_t>(blocks_for(work, 256), 148 * 16), 256, 0, s>>>(M, n, tau_min);
+    k_spm_init<<<std::min<size_t>(blocks_for(work, 256), static_cast<size_t>(device_sms()) * 16), 256, 0, s>>>(M, n, tau_min);
 }
 
 void launch_rng_script(uint32_t kind, uint64_t seed, uint64_t it, uint64_t ant, int derive,

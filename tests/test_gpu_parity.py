@@ -391,3 +391,14 @@ def test_non_integer_beta_lean_kernel(acs, orc, gpu):
     o = orc.run(I, m=1, iterations=3, seed=3, mode=O.SEQ, want_tau=True, beta=2.5, rng=O.PHILOX)
     assert st["global_best_len"].tolist() == o["trace"].tolist()
     assert np.array_equal(tau.view(np.uint64), o["tau"].view(np.uint64))
+
+
+@pytest.mark.parametrize("m", [198, 9000])
+def test_spm_sync_device_wide_sort(acs, orc, gpu, monkeypatch, m):
+    """SYNC x SELECTIVE above one CTA's sort (m > 8192): the step's
+    record operations are radix-sorted device-wide; forced for m = 198 too
+    (ACS_SSYNC_WIDE).  Bit-exact with the oracle either way."""
+    monkeypatch.setenv("ACS_SSYNC_WIDE", "1")
+    I = O.load("d198")
+    r = pair(acs, orc, I, "sync", O.SELECTIVE, m=m, iters=1 if m > 1000 else 3, seed=7)
+    check_exact(*r, O.SELECTIVE)
