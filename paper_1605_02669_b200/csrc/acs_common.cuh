@@ -10,7 +10,10 @@
 namespace acs_dev {
 
 
-constexpr int kBlock = 64;            // 2 ants per CTA: fine-grained spread over 148 SMs
+#ifndef ACS_BLOCK
+#define ACS_BLOCK 64
+#endif
+constexpr int kBlock = ACS_BLOCK;     // 2 ants per CTA: fine-grained spread over 148 SMs
 #ifndef ACS_MAXREGS
 #define ACS_MAXREGS 96
 #endif
