@@ -1,16 +1,14 @@
 #!/bin/bash
 # End-of-round pass on the GPU box: tests, smoke, headline bench + launch list
-# + ncu captures, setup-path timing against the reference code, and the
-# spm-sync quality leg.  Outputs under gpurun_out/.
+# + ncu captures (profile_round.sh), the reference arm, the two-rank bench path
+# (ranks sharing the GPU), setup timing.  Outputs under gpurun_out/.
 set -u
 mkdir -p gpurun_out
-R=${ROUND:-r01f}
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/tests_$R.log; tail -2 gpurun_out/tests_$R.log
+R=${ROUND:-r02f}
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/tests_$R.log; tail -2 gpurun_out/tests_$R.log
 timeout 600 python __graft_entry__.py > gpurun_out/smoke_$R.log 2>&1; tail -1 gpurun_out/smoke_$R.log
 ROUND=$R bash scripts/profile_round.sh
-timeout 1200 python scripts/setup_timing.py --out gpurun_out/setup_timing_$R.json > gpurun_out/setup_timing_$R.log 2>&1
-tail -8 gpurun_out/setup_timing_$R.log
-if [ "${QUALITY:-1}" = "1" ]; then
-  timeout 1500 python tools/quality.py --instances d198 pcb442 --variants spm-sync --seeds 30 --iterations 1000 \
-    --out gpurun_out/q_spm_sync_$R.json
-fi
+timeout 600 python bench.py --impl reference --steps 5 --warmup 2 > gpurun_out/bench_ref_$R.json 2> gpurun_out/bench_ref_$R.err
+tail -c 800 gpurun_out/bench_ref_$R.json
+bash scripts/multirank.sh
+python scripts/create_timing.py --instance pr2392 > gpurun_out/create_$R.log 2>&1; cat gpurun_out/create_$R.log
