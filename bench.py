@@ -499,7 +499,7 @@ def e2e(P, inst, params, args, world, dist=None, device=0, shared=False):
     region (acs_gpu_island_exchange over NCCL; host exchange over gloo when
     ranks share a GPU); the NCCL communicator setup (acs_gpu_island_init, the
     analogue of init_process_group) is excluded from the wall time.  The
-    whole-job value uses the max wall time over ranks.  Repeated 3 times (host
+    whole-job value uses the max wall time over ranks.  Repeated 5 times (host
     wall clocks on the box jitter by tens of ms); the median is reported."""
     import ctypes as C
     import numpy as np
@@ -546,7 +546,7 @@ def e2e(P, inst, params, args, world, dist=None, device=0, shared=False):
 
     one(1)  # untimed: lazy CUDA module loading of the setup kernels
     walls = []
-    for _ in range(3):
+    for _ in range(5):
         if dist:
             dist.barrier()
         dt = one(K)
@@ -567,7 +567,7 @@ def e2e(P, inst, params, args, world, dist=None, device=0, shared=False):
                       + ("acs_gpu_island_exchange over NCCL" if nccl else "host exchange over gloo") + ")"
                       if world > 1 else "")
                    + f" + acs_gpu_get_best + acs_gpu_destroy, host buffers, on each of {world} rank(s); "
-                   f"max wall over ranks, median of 3 runs",
+                   f"max wall over ranks, median of 5 runs",
             "nccl_comm_nranks": world if nccl else None,
             "wall_s": round(dt, 4), "wall_s_runs": [round(w, 4) for w in walls]}
 

@@ -755,7 +755,8 @@ __device__ __forceinline__ void st_u32_if(bool p, uint32_t *ptr, uint32_t v) {
 // cases (c = 0, 1, >= 2) picked by selects -- no branch on the chain.
 constexpr uint32_t kLeanPwHi = 64;  // c < 512 * 64 pending updates (m <= 31744)
 __device__ __forceinline__ double trail_value_sel(double b, uint32_t c, const DevColony &C, const double *pw) {
-    const double p = __dmul_rn(pw[c & 511u], pw[512u + min(c >> 9, kLeanPwHi - 1)]);
+    // c < 512 * kLeanPwHi: the launcher runs this kernel only for m <= that
+    const double p = __dmul_rn(pw[c & 511u], pw[512u + (c >> 9)]);
     const double one = affine(b, C.c_l, C.c_0);
     const double closed = __dadd_rn(C.tau_min, __dmul_rn(p, __dsub_rn(b, C.tau_min)));
     const double x = c >= 2u ? closed : one;
@@ -927,7 +928,11 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             // RNG: commit a greedy step's q draw, peek the next one
             if (greedy && cand) rng.advance();
             la.prepare(rng);
-            route_put(route, rbuf, t, v, lane);
+            {   // route buffered in registers, one 128 B store per 32 steps
+                const uint32_t tl5 = t & 31u;
+                if (static_cast<uint32_t>(lane) == tl5) rbuf = v;
+                if (tl5 == 31u) route[(t & ~31u) + lane] = rbuf;
+            }
             cur = v;
             __syncwarp();
         }
