@@ -281,9 +281,10 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        if not shared:  # NCCL's own init lines carry the communicator size (nRanks)
+        if not shared:  # NCCL's own init lines carry the communicator size (nRanks), on stderr
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if shared:
             dist.init_process_group("gloo")
         else:
