@@ -1227,11 +1227,25 @@ __device__ __forceinline__ void st_relaxed_u32_if(bool p, uint32_t *ptr, uint32_
 // f(tau_old), the value the selection read.  Returns hit.
 template <bool kKeep>
 __device__ __forceinline__ bool spm8_update(const DevColony &C, unsigned char *rb, uint32_t nb, double tau_old,
-                                            uint32_t &idl, double &val, uint32_t &tail, int lane) {
+                                            uint32_t &idl, double &val, uint32_t &tail, int lane,
+                                            uint32_t *stale = nullptr) {
     const unsigned m = __ballot_sync(kFull, idl == nb);
     const bool hit = m != 0u;
     const uint32_t t = (tail + 1) & 7u;
     const uint32_t slot = hit ? static_cast<uint32_t>(__ffs(m) - 1) : t;
+#ifdef ACS_COUNT_LOST
+    // instrumented build: the update works from a copy of the record read at
+    // the start of the step; stale if another ant changed its tail or the
+    // updated slot's id since
+    {
+        const uint32_t cid = __shfl_sync(kFull, idl, static_cast<int>(slot));
+        if (stale && lane == 0) {
+            const uint32_t mt = ld_relaxed_u32(reinterpret_cast<const uint32_t *>(rb + kRec8Tail));
+            const uint32_t mid = ld_relaxed_u32(reinterpret_cast<const uint32_t *>(rb + kRec8Ids) + slot);
+            *stale += (mt != tail || mid != cid) ? 1u : 0u;
+        }
+    }
+#endif
     const double hv = kKeep ? __shfl_sync(kFull, val, static_cast<int>(slot)) : tau_old;
     const double y = affine(hit ? hv : C.tau_min, C.c_l, C.c_0);
     const bool l0 = lane == 0;
@@ -1383,8 +1397,14 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
             // ---- off the chain: record cur's two ordered updates
             // (hits are derived at the tour end: 2 record operations per update)
             unsigned char *rb = rec8(C, cur);
-            if (prev != kEmpty) wc.misses += !spm8_update<true>(C, rb, prev, 0.0, ridl, rval, rtail, lane);
-            wc.misses += !spm8_update<false>(C, rb, v, tau_old, ridl, rval, rtail, lane);
+#ifdef ACS_COUNT_LOST
+            uint32_t *stale = &wc.lost;  // counted by lane 0, as the updates
+            if (lane == 0) wc.writes += (prev != kEmpty) ? 2 : 1;
+#else
+            uint32_t *stale = nullptr;
+#endif
+            if (prev != kEmpty) wc.misses += !spm8_update<true>(C, rb, prev, 0.0, ridl, rval, rtail, lane, stale);
+            wc.misses += !spm8_update<false>(C, rb, v, tau_old, ridl, rval, rtail, lane, stale);
             prev = cur;
             const bool me = lane == pos;
             sts_if(me, vw, word | bit);

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Lost-update rate of the RELAXED construction (ACS-GPU-Alt) against the
-number of ants in flight.  Needs the instrumented library
+number of ants in flight (--variant spm: the share of selective-record
+updates made from a stale copy of the record).  Needs the instrumented library
 (make ab V=lost DEFS=-DACS_COUNT_LOST): every relaxed pheromone write is an
 exchange, and a write whose old value differs from the value its update read
 overwrote (lost) another ant's update.
@@ -17,13 +18,13 @@ import sys
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def child(instances, iters, seed):
+def child(instances, iters, seed, variant):
     sys.path.insert(0, REPO)
     import paper_1605_02669_b200 as P
     out = {}
     for name in instances:
         inst = P.load_instance(name)
-        with P.Colony(inst, P.AcsParams(variant="relaxed", seed=seed, rng="philox")) as col:
+        with P.Colony(inst, P.AcsParams(variant=variant, seed=seed, rng="philox")) as col:
             st = col.iterate(iters)
             c = col.counters()
         opt = inst.optimum
@@ -40,16 +41,18 @@ def main():
     ap.add_argument("--resident", nargs="+", type=int, default=[0, 128, 6])
     ap.add_argument("--iterations", type=int, default=100)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--variant", default="relaxed", help="relaxed: lost trail updates; spm: stale record updates")
     ap.add_argument("--child", action="store_true")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     if a.child:
-        return child(a.instances, a.iterations, a.seed)
+        return child(a.instances, a.iterations, a.seed, a.variant)
     res = {"params": vars(a), "results": {}}
     for w in a.resident:
         env = dict(os.environ, ACS_LIB_VARIANT="lost", ACS_RESIDENT_ANTS=str(w))
         r = subprocess.run([sys.executable, __file__, "--child", "--instances", *a.instances, "--iterations",
-                            str(a.iterations), "--seed", str(a.seed)], env=env, capture_output=True, text=True)
+                            str(a.iterations), "--seed", str(a.seed), "--variant", a.variant], env=env,
+                           capture_output=True, text=True)
         if r.returncode:
             print(r.stderr[-2000:])
             continue
