@@ -18,7 +18,7 @@ for f in sorted(glob.glob("gpurun_out/tput/*.json")):
         continue
     r = d["roofline"]
     rows.append((d["config"]["instance"], d["config"]["variant"], d["ms_per_step"], d["value"],
-                 r["latency"]["frac"], r["frac"]))
+                 r["latency"]["frac"], r["latency"]["isolated_ant"]["frac_colony"], r["frac"]))
 for x in rows:
-    print("%-8s %-9s %8.3f ms/it %12.0f tours/s  latency %.2f  hbm %.3f" % x)
+    print("%-8s %-9s %8.3f ms/it %12.0f tours/s  floor frac %.2f  isolated-ant frac %.2f  l2 %.3f" % x)
 PY
