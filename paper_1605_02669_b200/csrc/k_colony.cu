@@ -1225,14 +1225,28 @@ __device__ __forceinline__ void st_relaxed_u32_if(bool p, uint32_t *ptr, uint32_
 // f(tau_min) into slot (tail + 1) % 8 with its id, and the tail.  kKeep: the
 // copy stays current for a following update; otherwise a hit's new value is
 // f(tau_old), the value the selection read.  Returns hit.
+// The same with the hit already known (hit: slot hslot holds nb): the lean
+// step knows both from its lookup, so no ballot is spent on them.
+template <bool kKeep>
+__device__ __forceinline__ bool spm8_update_at(const DevColony &C, unsigned char *rb, uint32_t nb, double tau_old,
+                                               bool hit, uint32_t hslot, uint32_t &idl, double &val, uint32_t &tail,
+                                               int lane, uint32_t *stale = nullptr);
+
 template <bool kKeep>
 __device__ __forceinline__ bool spm8_update(const DevColony &C, unsigned char *rb, uint32_t nb, double tau_old,
                                             uint32_t &idl, double &val, uint32_t &tail, int lane,
                                             uint32_t *stale = nullptr) {
     const unsigned m = __ballot_sync(kFull, idl == nb);
-    const bool hit = m != 0u;
+    return spm8_update_at<kKeep>(C, rb, nb, tau_old, m != 0u, m ? static_cast<uint32_t>(__ffs(m) - 1) : 0u, idl, val,
+                                 tail, lane, stale);
+}
+
+template <bool kKeep>
+__device__ __forceinline__ bool spm8_update_at(const DevColony &C, unsigned char *rb, uint32_t nb, double tau_old,
+                                               bool hit, uint32_t hslot, uint32_t &idl, double &val, uint32_t &tail,
+                                               int lane, uint32_t *stale) {
     const uint32_t t = (tail + 1) & 7u;
-    const uint32_t slot = hit ? static_cast<uint32_t>(__ffs(m) - 1) : t;
+    const uint32_t slot = hit ? hslot : t;
 #ifdef ACS_COUNT_LOST
     // instrumented build: the update works from a copy of the record read at
     // the start of the step; stale if another ant changed its tail or the
@@ -1337,7 +1351,8 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
             const bool unv = !(word & bit);
             // pending update of record cur with prev: a miss evicts slot (tail+1) % S
             const bool pend = prev != kEmpty;
-            const bool pmiss = pend && __ballot_sync(kFull, rec.idl == prev) == 0u;
+            const unsigned pm = __ballot_sync(kFull, pend && rec.idl == prev);  // prev's slot, if any
+            const bool pmiss = pend && pm == 0u;
             const int evict = pmiss ? static_cast<int>((rec.tail + 1) & 7u) : -1;
             int hit = rec.find(c);
             if (hit == evict) hit = -1;
@@ -1363,6 +1378,7 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
                 }
             }
             double tau_old = 0.0;
+            int vslot = -1;  // v's slot in record cur after the pending update (candidate steps)
             if (!cand) {  // fallback: the record after its pending update, then the scan
                 if (pend) {
                     wc.misses += !spm8_update<true>(C, rec8(C, cur), prev, 0.0, rec.idl, rec.val, rec.tail, lane);
@@ -1387,6 +1403,7 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
                 wc.fb_elems += n - t;
             } else {
                 tau_old = __shfl_sync(kFull, tv, pos);
+                vslot = __shfl_sync(kFull, hit, pos);
             }
             // record cur's lane-distributed slots: all its two updates need
             uint32_t ridl = rec.idl, rtail = rec.tail;
@@ -1403,8 +1420,14 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
 #else
             uint32_t *stale = nullptr;
 #endif
-            if (prev != kEmpty) wc.misses += !spm8_update<true>(C, rb, prev, 0.0, ridl, rval, rtail, lane, stale);
-            wc.misses += !spm8_update<false>(C, rb, v, tau_old, ridl, rval, rtail, lane, stale);
+            // the lookup already located both neighbours: prev by the step's
+            // first ballot, v (candidate step) by the winning lane's find
+            if (prev != kEmpty)
+                wc.misses += !spm8_update_at<true>(C, rb, prev, 0.0, pm != 0u, pm ? static_cast<uint32_t>(__ffs(pm) - 1) : 0u,
+                                                   ridl, rval, rtail, lane, stale);
+            if (cand) wc.misses += !spm8_update_at<false>(C, rb, v, tau_old, vslot >= 0, static_cast<uint32_t>(vslot), ridl,
+                                                          rval, rtail, lane, stale);
+            else wc.misses += !spm8_update<false>(C, rb, v, tau_old, ridl, rval, rtail, lane, stale);
             prev = cur;
             const bool me = lane == pos;
             sts_if(me, vw, word | bit);
