@@ -884,6 +884,10 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
                 ++wc.fallback;
                 wc.fb_elems += n - t;
             }
+            // this edge's length share, formed before the next row's loads: the
+            // row's d must not stay live across them (ptxas would copy the
+            // reloaded register at the loop end and wait there for the load)
+            const int32_t dme = lane == pos ? dl : 0;
             // ---- next row: issued as soon as v is known
             ri = static_cast<size_t>(v) * 32 + lane;
             el = __ldg(C.rows + ri);
@@ -924,7 +928,7 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             // visited mark: the winning lane stores the word it tested (pos = -1
             // after a fallback, which marked v itself)
             sts_if(me, vw, word | bit);
-            lenl += me ? dl : 0;
+            lenl += dme;
             // RNG: commit a greedy step's q draw, peek the next one
             if (greedy && cand) rng.advance();
             la.prepare(rng);
