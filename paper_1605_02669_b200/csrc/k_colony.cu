@@ -1412,6 +1412,7 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
             // record cur's lane-distributed slots: all its two updates need
             uint32_t ridl = rec.idl, rtail = rec.tail;
             double rval = rec.val;
+            const int32_t dme = lane == pos ? dl : 0;  // before the loads (as k_tour_lean)
             // ---- next row and record: issued as soon as v is known
             el = __ldg(C.rows + static_cast<size_t>(v) * 32 + lane);
             rec.load(rec8(C, v), lane);
@@ -1435,9 +1436,7 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
             prev = cur;
             const bool me = lane == pos;
             sts_if(me, vw, word | bit);
-#ifndef ACS_X_LEN_PASS
-            lenl += me ? dl : 0;
-#endif
+            lenl += dme;
             if (greedy && cand) rng.advance();
             la.prepare(rng);
             route_put(route, rbuf, t, v, lane);
@@ -1461,9 +1460,7 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
         r2.load(rec8(C, start), lane);
         wc.misses += !spm8_update<true>(C, rec8(C, start), cur, 0.0, r2.idl, r2.val, r2.tail, lane);
         wc.hits = 2 * n - wc.misses;  // n local updates (k = 1), two record operations each
-#ifndef ACS_X_LEN_PASS
         if (lane == 0) C.lens[a] = len + dclose;
-#endif
         wc.flush(C.counters, lane, n - 1);
         __syncwarp();
     }
@@ -2305,9 +2302,6 @@ static void launch_spm_rng(const DevInstance &I, const DevColony &C, bool one_wa
                 launch_tour_kernel(k_construct_spm<8, RNG, true>, I, C, false, s);
 #else
                 launch_tour_kernel(k_spm_lean<RNG>, I, C, false, s);
-#ifdef ACS_X_LEN_PASS
-                launch_tour_lengths(I, C.routes, C.m, C.lens, s);
-#endif
 #endif
             }
             else launch_tour_kernel(k_construct_spm<8, RNG>, I, C, one_warp, s);
