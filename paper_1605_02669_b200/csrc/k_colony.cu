@@ -1,10 +1,13 @@
 // k_colony.cu -- per-iteration kernels of the ACS hot path (sm_100a).
 //
-//   K4 k_construct_dense   whole tour per launch, warp per ant, lane per candidate slot:
-//                          ATOMIC (CAS, CONSISTENT) / RELAXED (plain ld/st, ACS-GPU-Alt) /
-//                          SEQ (the same kernel on one warp = SPEC SEQ, bit-exact)
-//   K4 k_construct_spm     selective pheromone memory (ACS-GPU-SPM) / SPM SEQ
-//   K3 k_def_*             step-synchronous deferred variant (SPEC SYNC, bit-exact)
+//   K4 k_tour_lean         whole tour per launch, warp per ant, lane per candidate slot,
+//                          the paper's configuration (k = 1, 32-slot lists):
+//                          ATOMIC (red.add counters, CONSISTENT) / RELAXED (ACS-GPU-Alt)
+//   K4 k_construct_dense   the same for any k and list length; SEQ (one warp, bit-exact)
+//   K4 k_spm_lean          selective pheromone memory (ACS-GPU-SPM), k = 1, s = 8
+//   K4 k_construct_spm     the same for any k / s; SPM SEQ
+//   K3 k_deferred          step-synchronous deferred variant (SPEC SYNC, bit-exact)
+//   K3 k_ssync_*           SYNC x SELECTIVE (spm-sync, bit-exact)
 //   K7 k_best              select_best (ties -> lowest ant) + strict is_better + stats
 //   K7 k_global_*          global update on the global-best edges only (D3)
 //
@@ -554,17 +557,6 @@ __device__ __forceinline__ bool copy_index(uint32_t n, uint32_t u, uint32_t v, i
     return lane < 4 && (dense || col < 32u);
 }
 
-// copy_index for k = 1 and lanes 0-2 only (lane 3's copy is written a step
-// late by the row-v lane): no mirror operand
-__device__ __forceinline__ bool copy3_index(uint32_t n, uint32_t u, uint32_t v, int pos, int lane,
-                                            bool &dense, size_t &idx) {
-    // select-only form (no branches): row = u for even lanes, v for lane 1
-    const uint32_t row = (lane & 1) ? v : u;
-    dense = !(lane & 2);
-    const uint32_t col = dense ? (u ^ v ^ row) : static_cast<uint32_t>(pos);
-    idx = static_cast<size_t>(row) * (dense ? n : 32u) + col;
-    return lane < 2 || (lane == 2 && pos >= 0);
-}
 
 // kMode 0 = RELAXED (ACS-GPU-Alt): plain relaxed stores of f(tau_old), lost
 //           updates allowed; also SEQ when launched on one warp.
@@ -572,10 +564,9 @@ __device__ __forceinline__ bool copy3_index(uint32_t n, uint32_t u, uint32_t v, 
 //           `red.add` on a per-copy counter -- no update can be lost and no
 //           ant ever waits on an atomic -- and readers see f^c(base).  The
 //           iteration epilogue folds the counters back into the bases.
-// kLean: the paper's configuration (k = 1, 32-slot candidate lists) compiled
-// without the update-period counter and the list-length tests, and with the
-// k = 1 copy addressing specialised (lanes 0-2, no mirror operand).
-template <int kMode, class RNG, int kRegs = kMaxRegs, bool kLean = false>
+// The general kernel (any update period k, lists of up to 32 slots, one warp
+// for SEQ); the paper's configuration (k = 1, 32-slot lists) runs k_tour_lean.
+template <int kMode, class RNG, int kRegs = kMaxRegs>
 __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C) {
     constexpr bool kAtomic = kMode == 1;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -626,13 +617,13 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
             // Its operands depend on the row only, so they are formed here, off
             // the selection chain, and the store is issued after the next
             // row's loads.
-            const bool mw = (kLean || static_cast<uint32_t>(lane) < C.L) && (el.x & kIdMask) == mprev;
+            const bool mw = static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev;
             const size_t mi = static_cast<size_t>(cur) * 32 + lane;
             const double mval = kAtomic ? 0.0 : affine(tl, C.c_l, C.c_0);
             Step st;
             if constexpr (kAtomic) {
                 const double tv = trail_value(tl, cl, C, pw_lo, pw_hi);
-                select_step<false, kLean>(I, C, vis, cur, el, tv, rng, la, scratch, lane,
+                select_step<false>(I, C, vis, cur, el, tv, rng, la, scratch, lane,
                             [&](uint32_t v, bool act) {
                                 if (!act) return 0.0;
                                 const size_t k = static_cast<size_t>(cur) * n + v;
@@ -641,7 +632,7 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
                             },
                             st);
             } else {
-                select_step<false, kLean>(I, C, vis, cur, el, tl, rng, la, scratch, lane,
+                select_step<false>(I, C, vis, cur, el, tl, rng, la, scratch, lane,
                             [&](uint32_t v, bool act) {
                                 return act ? ld_relaxed(C.tau + static_cast<size_t>(cur) * n + v) : 0.0;
                             },
@@ -662,14 +653,13 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
             }
             mprev = kEmpty;
             if (st.kind) wc.count(st.kind, n - t);  // greedy steps are derived at flush
-            if (kLean || ++kc == C.k) {  // D9 per-ant edge counter (warp-uniform)
+            if (++kc == C.k) {  // D9 per-ant edge counter (warp-uniform)
                 kc = 0;
-                if constexpr (!kLean) ++wc.updates;
+                ++wc.updates;
                 bool dense;
                 size_t k;
                 // lanes 0-2 now; lane 3's copy (tauc[v][mirror]) one step late, above
-                if (kLean ? copy3_index(n, cur, st.v, st.pos, lane, dense, k)
-                          : (lane < 3 && copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k))) {
+                if (lane < 3 && copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k)) {
                     if constexpr (kAtomic) red_add1((dense ? C.cnt : C.cntc) + k);
                     else st_relaxed((dense ? C.tau : C.tauc) + k, affine(st.tau_old, C.c_l, C.c_0));
                 }
@@ -686,7 +676,6 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
             __syncwarp();
         }
         route_flush(route, rbuf, n - 1, lane);
-        if constexpr (kLean) wc.updates += n - 1;
         // last step's deferred mirror copy (el/tl hold row `cur`)
         if (static_cast<uint32_t>(lane) < C.L && (el.x & kIdMask) == mprev) {
             if constexpr (kAtomic) red_add1(C.cntc + static_cast<size_t>(cur) * 32 + lane);
@@ -1130,9 +1119,9 @@ struct SpmRec {
     }
 };
 
-// kLean: k = 1 and 32-slot lists (as the dense kernel): no period counter,
-// no list-length tests on the step path
-template <int S, class RNG, bool kLean = false>
+// The general selective kernel (any k, s, list length; one warp for SPM SEQ);
+// the paper's configuration (k = 1, 32-slot lists, s = 8) runs k_spm_lean.
+template <int S, class RNG>
 __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1168,11 +1157,11 @@ __global__ void __maxnreg__(kMaxRegs) k_construct_spm(DevInstance I, DevColony C
             }
             const double tau_lane = rec.lookup(el.x & kIdMask, C.tau_min);
             Step st;
-            select_step<false, kLean>(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
+            select_step<false>(I, C, vis, cur, el, tau_lane, rng, la, scratch, lane,
                         [&](uint32_t v, bool act) { return rec.lookup(act ? v : kEmpty, C.tau_min); }, st);
             wc.count(st.kind, n - t);
             el = __ldg(C.rows + static_cast<size_t>(st.v) * 32 + lane);  // next row first
-            pending = kLean || (++kc == C.k);
+            pending = ++kc == C.k;
             if (pending) {
                 kc = 0;
                 ++wc.updates;
@@ -2241,11 +2230,8 @@ constexpr int kWideRegs = 72;
 
 template <int kMode, class RNG, int kRegs, bool kLean>
 constexpr auto dense_kernel() {
-#ifndef ACS_X_OLD_LEAN
     if constexpr (kLean) return k_tour_lean<kMode, RNG, kRegs>;
-    else
-#endif
-        return k_construct_dense<kMode, RNG, kRegs, kLean>;
+    else return k_construct_dense<kMode, RNG, kRegs>;
 }
 
 template <int kMode, class RNG, bool kLean>
@@ -2280,11 +2266,7 @@ static void launch_dense_t(const DevInstance &I, const DevColony &C, bool one_wa
 template <int kMode, class RNG>
 static void launch_dense(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw = false) {
     if (C.k == 1 && C.L == 32 && !one_warp && (!pw || C.pw_hi_n <= kLeanPwHi)) {
-#ifdef ACS_X_OLD_LEAN
-        launch_dense_t<kMode, RNG, true>(I, C, one_warp, s, pw);
-#else
         launch_dense_t<kMode, RNG, true>(I, C, one_warp, s, false);  // k_tour_lean: static power tables
-#endif
         return;
     }
     launch_dense_t<kMode, RNG, false>(I, C, one_warp, s, pw);
@@ -2297,13 +2279,7 @@ static void launch_spm_rng(const DevInstance &I, const DevColony &C, bool one_wa
         case 2: launch_tour_kernel(k_construct_spm<2, RNG>, I, C, one_warp, s); break;
         case 4: launch_tour_kernel(k_construct_spm<4, RNG>, I, C, one_warp, s); break;
         case 8:
-            if (C.k == 1 && C.L == 32 && !one_warp) {
-#ifdef ACS_X_OLD_SPM
-                launch_tour_kernel(k_construct_spm<8, RNG, true>, I, C, false, s);
-#else
-                launch_tour_kernel(k_spm_lean<RNG>, I, C, false, s);
-#endif
-            }
+            if (C.k == 1 && C.L == 32 && !one_warp) launch_tour_kernel(k_spm_lean<RNG>, I, C, false, s);
             else launch_tour_kernel(k_construct_spm<8, RNG>, I, C, one_warp, s);
             break;
         default: launch_tour_kernel(k_construct_spm<16, RNG>, I, C, one_warp, s); break;
