@@ -1310,7 +1310,6 @@ struct Rec8 {
 // 96 registers: 5 warps per SM sub-partition (16K registers each), so m = n = 2392 is one wave
 template <class RNG>
 __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C) {
-    constexpr int S = 8;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
@@ -1395,7 +1394,9 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
                 ++wc.fallback;
                 wc.fb_elems += n - t;
             } else {
+#ifdef ACS_COUNT_LOST
                 tau_old = __shfl_sync(kFull, tv, pos);
+#endif
                 vslot = __shfl_sync(kFull, hit, pos);
             }
             // record cur's lane-distributed slots: all its two updates need
@@ -1416,12 +1417,40 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
 #endif
             // the lookup already located both neighbours: prev by the step's
             // first ballot, v (candidate step) by the winning lane's find
+#ifndef ACS_COUNT_LOST
+            if (cand) {
+                // both updates at once, each by the lane owning its slot: the
+                // owner holds the slot's value, so no shuffle; a slot written
+                // twice (v's miss evicting prev's slot) is written by one lane
+                // in program order, prev's update first (D4)
+                const bool phit = pm != 0u, vhit = vslot >= 0;
+                const uint32_t e1 = (rtail + 1) & 7u;
+                const uint32_t s1 = !pend ? 32u : (phit ? static_cast<uint32_t>(__ffs(pm) - 1) : e1);
+                const uint32_t tail1 = (pend && !phit) ? e1 : rtail;
+                const uint32_t e2 = (tail1 + 1) & 7u;
+                const uint32_t s2 = vhit ? static_cast<uint32_t>(vslot) : e2;
+                const bool o1 = static_cast<uint32_t>(lane) == s1, o2 = static_cast<uint32_t>(lane) == s2;
+                const double y1 = affine(phit ? rval : C.tau_min, C.c_l, C.c_0);
+                const double y2 = affine(vhit ? rval : C.tau_min, C.c_l, C.c_0);
+                double *vp = reinterpret_cast<double *>(rb) + lane;
+                uint32_t *ip = reinterpret_cast<uint32_t *>(rb + kRec8Ids) + lane;
+                st_relaxed_if(o1, vp, y1);
+                st_relaxed_u32_if(o1 && !phit, ip, prev);
+                st_relaxed_if(o2, vp, y2);
+                st_relaxed_u32_if(o2 && !vhit, ip, v);
+                st_relaxed_u32_if(lane == 0 && ((pend && !phit) || !vhit), reinterpret_cast<uint32_t *>(rb + kRec8Tail),
+                                  vhit ? tail1 : e2);
+                wc.misses += static_cast<uint32_t>(pend && !phit) + static_cast<uint32_t>(!vhit);
+            } else
+                wc.misses += !spm8_update<false>(C, rb, v, tau_old, ridl, rval, rtail, lane, stale);
+#else
             if (prev != kEmpty)
                 wc.misses += !spm8_update_at<true>(C, rb, prev, 0.0, pm != 0u, pm ? static_cast<uint32_t>(__ffs(pm) - 1) : 0u,
                                                    ridl, rval, rtail, lane, stale);
             if (cand) wc.misses += !spm8_update_at<false>(C, rb, v, tau_old, vslot >= 0, static_cast<uint32_t>(vslot), ridl,
                                                           rval, rtail, lane, stale);
             else wc.misses += !spm8_update<false>(C, rb, v, tau_old, ridl, rval, rtail, lane, stale);
+#endif
             prev = cur;
             const bool me = lane == pos;
             sts_if(me, vw, word | bit);
