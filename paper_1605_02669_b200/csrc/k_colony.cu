@@ -180,6 +180,12 @@ __device__ __forceinline__ void finish_scan(const DevInstance &I, const DevColon
 // nodes, ties -> lowest id, no RNG draw (P1).  An exact pruned pass first; if
 // it cannot decide, the full scan -- or, with kDefer (the deferred kernel),
 // o.kind = 3: the caller's CTA runs the full scan cooperatively.
+#ifndef ACS_EXT_BATCH
+#define ACS_EXT_BATCH 2  // free-running kernels
+#endif
+#ifndef ACS_EXT_BATCH_DEFER
+#define ACS_EXT_BATCH_DEFER 3  // the lockstep kernel: its step waits for the slowest fallback
+#endif
 template <bool kDefer = false, class TauFn>
 __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevColony &C,
                                               const uint32_t *vis, uint32_t cur, TauFn tau_of,
@@ -214,30 +220,53 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
                 have = true; bs = __dmul_rn(tv, e); bv = v; bt = tv;
             }
         }
-        for (uint32_t base = 0; base < C.ext_len; base += 32) {
-            if (base) q = __ldg(xrow + base + lane);
-            const bool in_list = q.x != kEmpty;
-            const uint32_t qid = q.x & kIdMask;
-            const bool act = in_list && !visited(vis, qid);
-            const double tv = tau_of(in_list ? qid : 0u, act);
-            if (act) {
-                const double sc = __dmul_rn(tv, __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z)));
-                if (!have || sc > bs || (sc == bs && qid < bv)) {
-                    have = true; bs = sc; bv = qid; bt = tv; bm = q.x >> 24;
-                }
+        // kExtBatch slices per round trip: their id loads, then their trail
+        // loads, are issued together; the slices are still decided one by one
+        // in distance order, so the result is the slice-at-a-time walk's (a
+        // fallback that walks the whole list pays ceil(slices / kExtBatch)
+        // pairs of dependent L2 trips instead of one pair per slice)
+        constexpr uint32_t kExtBatch = kDefer ? ACS_EXT_BATCH_DEFER : ACS_EXT_BATCH;
+        for (uint32_t base = 0; base < C.ext_len; base += 32 * kExtBatch) {
+            uint4 qs[kExtBatch];
+            qs[0] = base ? __ldg(xrow + base + lane) : q;
+#pragma unroll
+            for (uint32_t j = 1; j < kExtBatch; ++j)
+                qs[j] = base + 32 * j < C.ext_len ? __ldg(xrow + base + 32 * j + lane) : make_uint4(kEmpty, 0u, 0u, 0u);
+            double tvs[kExtBatch];
+            bool acts[kExtBatch];
+#pragma unroll
+            for (uint32_t j = 0; j < kExtBatch; ++j) {
+                const bool in_list = qs[j].x != kEmpty;
+                const uint32_t qid = qs[j].x & kIdMask;
+                acts[j] = in_list && !visited(vis, qid);
+                tvs[j] = tau_of(in_list ? qid : 0u, acts[j]);
             }
-            double sb = bs;
-            uint32_t node = have ? bv : 0xffffffffu;
-            warp_argmax_node(sb, node, have);
-            // the list ends inside this slice: every non-candidate node was scanned
-            const bool exhausted = __any_sync(kFull, !in_list);
-            const uint32_t lw = __shfl_sync(kFull, q.w, 31), lz = __shfl_sync(kFull, q.z, 31);
-            const double bound = __dmul_rn(C.tau_bound, __hiloint2double(static_cast<int>(lw), static_cast<int>(lz)));
-            if (node != 0xffffffffu && (exhausted || bound < sb)) {
-                const unsigned owner = __ballot_sync(kFull, have && bv == node);
-                const int src = __ffs(owner) - 1;
-                finish_scan(I, C, cur, node, __shfl_sync(kFull, bt, src), lane, o, __shfl_sync(kFull, bm, src));
-                return;
+#pragma unroll
+            for (uint32_t j = 0; j < kExtBatch; ++j) {
+                const uint4 qj = qs[j];
+                const bool in_list = qj.x != kEmpty;
+                const uint32_t qid = qj.x & kIdMask;
+                const double tv = tvs[j];
+                if (acts[j]) {
+                    const double sc = __dmul_rn(tv, __hiloint2double(static_cast<int>(qj.w), static_cast<int>(qj.z)));
+                    if (!have || sc > bs || (sc == bs && qid < bv)) {
+                        have = true; bs = sc; bv = qid; bt = tv; bm = qj.x >> 24;
+                    }
+                }
+                double sb = bs;
+                uint32_t node = have ? bv : 0xffffffffu;
+                warp_argmax_node(sb, node, have);
+                // the list ends inside this slice: every non-candidate node was scanned
+                const bool exhausted = __any_sync(kFull, !in_list);
+                const uint32_t lw = __shfl_sync(kFull, qj.w, 31), lz = __shfl_sync(kFull, qj.z, 31);
+                const double bound = __dmul_rn(C.tau_bound, __hiloint2double(static_cast<int>(lw), static_cast<int>(lz)));
+                if (node != 0xffffffffu && (exhausted || bound < sb)) {
+                    const unsigned owner = __ballot_sync(kFull, have && bv == node);
+                    const int src = __ffs(owner) - 1;
+                    finish_scan(I, C, cur, node, __shfl_sync(kFull, bt, src), lane, o, __shfl_sync(kFull, bm, src));
+                    return;
+                }
+                if (base + 32 * j < C.ext_len) q = qj;  // the ring stage starts past the last slice
             }
         }
         // Past the ext rows: rings of grid cells around cur, nearest first.
