@@ -3,6 +3,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/grid_barrier tools/micro/grid_barrier.cu
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <cstdlib>
 namespace cg = cooperative_groups;
 
 constexpr unsigned kGroups = 8;
@@ -63,9 +64,32 @@ __device__ __forceinline__ void sync_acqrel(unsigned *bar, unsigned nblocks) {
     __syncthreads();
 }
 
+// monotonic counter: arrival is a non-returning red.release (no round trip),
+// every CTA polls with ld.acquire until the count reaches this generation's
+// target (the counter is never reset: target = (generation + 1) * nblocks)
+__device__ __forceinline__ void sync_mono(unsigned *bar, unsigned nblocks, unsigned &target) {
+    __syncthreads();
+    target += nblocks;
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 64) : "memory");
+        unsigned cur, spins = 0;
+        do { asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 64) : "memory"); }
+        while (static_cast<int>(cur - target) < 0 && ++spins < (1u << 24));
+        if (spins >= (1u << 24)) bar[96] = 1;  // watchdog: report instead of hanging
+    }
+    __syncthreads();
+}
+
 __global__ void k_bar(unsigned *bar, int mode, int iters, int sleep_ns) {
     cg::grid_group grid = cg::this_grid();
+    unsigned target = 0;
+    if (mode == 4) {  // resume from the counter's current generation
+        target = *reinterpret_cast<volatile unsigned *>(bar + 64);
+        target -= target % gridDim.x;
+        grid.sync();
+    }
     for (int i = 0; i < iters; ++i) {
+        if (mode == 4) { sync_mono(bar, gridDim.x, target); continue; }
         if (mode == 0) sync_two_level(bar, gridDim.x, sleep_ns);
         else if (mode == 1) sync_flat(bar, gridDim.x);
         else if (mode == 2) sync_acqrel(bar, gridDim.x);
@@ -73,16 +97,18 @@ __global__ void k_bar(unsigned *bar, int mode, int iters, int sleep_ns) {
     }
 }
 
-int main() {
+int main(int argc, char **argv) {
+    setvbuf(stdout, nullptr, _IONBF, 0);
+    const int mode_lo = argc > 1 ? atoi(argv[1]) : 0;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     unsigned *bar;
     cudaMalloc(&bar, 4096);
     cudaMemset(bar, 0, 4096);
     const int iters = 4784;
-    const char *names[] = {"two-level nanosleep(8)", "flat spin", "flat acq_rel", "cg::grid.sync"};
+    const char *names[] = {"two-level nanosleep(8)", "flat spin", "flat acq_rel", "cg::grid.sync", "mono red+poll"};
     for (int blk : {640, 128}) {
-        for (int mode = 0; mode < 4; ++mode) {
+        for (int mode = mode_lo; mode < 5; ++mode) {
             for (int sl : {8, 0}) {
                 if (mode != 0 && sl == 0) continue;
                 int grid = sms;
@@ -95,6 +121,9 @@ int main() {
                 cudaEventRecord(b);
                 cudaEventSynchronize(b);
                 float ms; cudaEventElapsedTime(&ms, a, b);
+                unsigned wd = 0;
+                cudaMemcpy(&wd, bar + 96, 4, cudaMemcpyDeviceToHost);
+                if (wd) printf("watchdog fired\n");
                 printf("block %4d %-24s sleep %d: %.3f us per barrier (%s)\n", blk, names[mode], mode ? -1 : sl,
                        ms * 1e3 / iters, cudaGetErrorString(cudaGetLastError()));
             }
