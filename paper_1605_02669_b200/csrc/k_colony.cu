@@ -181,7 +181,7 @@ __device__ __forceinline__ void finish_scan(const DevInstance &I, const DevColon
 // it cannot decide, the full scan -- or, with kDefer (the deferred kernel),
 // o.kind = 3: the caller's CTA runs the full scan cooperatively.
 #ifndef ACS_EXT_BATCH
-#define ACS_EXT_BATCH 2  // free-running kernels
+#define ACS_EXT_BATCH 1  // free-running kernels (2 and 3 measured within noise, +2 % instructions)
 #endif
 #ifndef ACS_EXT_BATCH_DEFER
 #define ACS_EXT_BATCH_DEFER 3  // the lockstep kernel: its step waits for the slowest fallback
