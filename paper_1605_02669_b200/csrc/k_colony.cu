@@ -917,32 +917,37 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             // prev writes the late mirror copy of the previous edge; the fourth
             // copy, tauc[v][mirror], is next step's late copy.
             const bool me = lane == pos;
-            if constexpr (kAtomic) {
-                red_add_if(me || mw, C.cntc + mi, one);
-                // the two dense counters in one instruction: lane pos bumps
-                // cnt[u][v], lane pos ^ 1 bumps cnt[v][u] (no value to move)
-                const bool mate = lane == (pos ^ 1);
-                const uint32_t row = me ? cur : v;
-                red_add_if(pos >= 0 && (me || mate), C.cnt + (static_cast<size_t>(row) * n + (cur ^ v ^ row)), one);
-            } else {
-                const size_t d_uv = static_cast<size_t>(cur) * n + v, d_vu = static_cast<size_t>(v) * n + cur;
+            // the pheromone update stores; ATOMIC issues them after the RNG and
+            // route work, RELAXED before it (each order measured ~1 % faster
+            // for its mode)
+            auto update_stores = [&]() {
+                if constexpr (kAtomic) {
+                    red_add_if(me || mw, C.cntc + mi, one);
+                    // the two dense counters in one instruction: lane pos bumps
+                    // cnt[u][v], lane pos ^ 1 bumps cnt[v][u] (no value to move)
+                    const bool mate = lane == (pos ^ 1);
+                    const uint32_t row = me ? cur : v;
+                    red_add_if(pos >= 0 && (me || mate), C.cnt + (static_cast<size_t>(row) * n + (cur ^ v ^ row)), one);
+                } else {
+                    const size_t d_uv = static_cast<size_t>(cur) * n + v, d_vu = static_cast<size_t>(v) * n + cur;
 #ifdef ACS_COUNT_LOST
-                // instrumented build: the candidate-copy write (the copy this lane
-                // read as tl) is an exchange; an old value other than tl means
-                // another ant's update of that trail landed in between and is lost
-                if (me || mw) {
-                    ++wc.writes;
-                    wc.lost += xchg_lost(C.tauc + mi, mval, told);
-                }
-                st_relaxed_if(me, C.tau + d_uv, mval);
-                st_relaxed_if(me, C.tau + d_vu, mval);
+                    // instrumented build: the candidate-copy write (the copy this lane
+                    // read as tl) is an exchange; an old value other than tl means
+                    // another ant's update of that trail landed in between and is lost
+                    if (me || mw) {
+                        ++wc.writes;
+                        wc.lost += xchg_lost(C.tauc + mi, mval, told);
+                    }
+                    st_relaxed_if(me, C.tau + d_uv, mval);
+                    st_relaxed_if(me, C.tau + d_vu, mval);
 #else
-                st_relaxed_if(me || mw, C.tauc + mi, mval);
-                st_relaxed_if(me, C.tau + d_uv, mval);
-                st_relaxed_if(me, C.tau + d_vu, mval);
+                    st_relaxed_if(me || mw, C.tauc + mi, mval);
+                    st_relaxed_if(me, C.tau + d_uv, mval);
+                    st_relaxed_if(me, C.tau + d_vu, mval);
 #endif
-            }
-            mprev = cur;
+                }
+            };
+            if constexpr (!kAtomic) update_stores();
             // visited mark: the winning lane stores the word it tested (pos = -1
             // after a fallback, which marked v itself)
             sts_if(me, vw, word | bit);
@@ -955,6 +960,8 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
                 if (static_cast<uint32_t>(lane) == tl5) rbuf = v;
                 if (tl5 == 31u) route[(t & ~31u) + lane] = rbuf;
             }
+            if constexpr (kAtomic) update_stores();
+            mprev = cur;
             cur = v;
             __syncwarp();
         }
@@ -1444,6 +1451,13 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
 #else
             uint32_t *stale = nullptr;
 #endif
+            // the step's other off-chain work first, then the record updates
+            // (measured 1 % faster than the reverse order)
+            sts_if(lane == pos, vw, word | bit);
+            lenl += dme;
+            if (greedy && cand) rng.advance();
+            la.prepare(rng);
+            route_put(route, rbuf, t, v, lane);
             // the lookup already located both neighbours: prev by the step's
             // first ballot, v (candidate step) by the winning lane's find
 #ifndef ACS_COUNT_LOST
@@ -1481,12 +1495,6 @@ __global__ void __maxnreg__(ACS_SPM_REGS) k_spm_lean(DevInstance I, DevColony C)
             else wc.misses += !spm8_update<false>(C, rb, v, tau_old, ridl, rval, rtail, lane, stale);
 #endif
             prev = cur;
-            const bool me = lane == pos;
-            sts_if(me, vw, word | bit);
-            lenl += dme;
-            if (greedy && cand) rng.advance();
-            la.prepare(rng);
-            route_put(route, rbuf, t, v, lane);
             cur = v;
             __syncwarp();
         }
