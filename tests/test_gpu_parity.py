@@ -244,16 +244,31 @@ def test_lean_kernel_small_colonies(acs, orc, gpu, variant, m):
     assert st["iter_best_len"].tolist()[-1] == lens.min()
 
 
-def test_lean_kernel_single_ant_pr2392(acs, orc, gpu):
-    """The headline instance through the lean kernel, one ant: bit-exact SEQ."""
+@pytest.mark.parametrize("variant", ["relaxed", "atomic", "spm"])
+def test_lean_kernel_single_ant_pr2392(acs, orc, gpu, variant):
+    """The headline instance through the lean kernels (k_tour_lean for
+    relaxed / atomic, k_spm_lean for spm), one ant: bit-exact SEQ (SEQ x
+    SELECTIVE for spm) -- trace, routes, and the whole pheromone matrix or the
+    selective records as bit patterns."""
     I = O.load("pr2392")
-    p = acs.AcsParams(variant="relaxed", m=1, seed=3, rng="philox")
+    p = acs.AcsParams(variant=variant, m=1, seed=3, rng="philox")
+    spm = variant == "spm"
     with acs.Colony(to_acs(acs, I), p) as col:
         st = col.iterate(2)
-        tau = col.pheromone()
-    o = orc.run(I, m=1, iterations=2, seed=3, mode=O.SEQ, want_tau=True, rng=O.PHILOX)
+        routes, lens = col.routes()
+        if spm:
+            ids, vals, tail = col.selective()
+        else:
+            tau = col.pheromone()
+    o = orc.run(I, m=1, iterations=2, seed=3, mode=O.SEQ, rng=O.PHILOX,
+                **({"memory": O.SELECTIVE, "want_spm": True} if spm else {"want_tau": True}))
     assert st["global_best_len"].tolist() == o["trace"].tolist()
-    assert np.array_equal(tau.view(np.uint64), o["tau"].view(np.uint64))
+    assert (routes == o["routes"]).all() and lens.tolist() == o["lengths"].tolist()
+    if spm:
+        assert (ids == o["spm_ids"]).all() and (tail == o["spm_tail"]).all()
+        assert np.array_equal(vals.view(np.uint64), o["spm_vals"].view(np.uint64))
+    else:
+        assert np.array_equal(tau.view(np.uint64), o["tau"].view(np.uint64))
 
 
 def test_sync_more_ants_than_resident_warps(acs, orc, gpu):
