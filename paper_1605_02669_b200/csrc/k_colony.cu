@@ -772,9 +772,11 @@ __device__ __forceinline__ void st_u32_if(bool p, uint32_t *ptr, uint32_t v) {
 // static shared tables, every operand formed unconditionally and the three
 // cases (c = 0, 1, >= 2) picked by selects -- no branch on the chain.
 constexpr uint32_t kLeanPwHi = 64;  // c < 512 * 64 pending updates (m <= 31744)
+template <bool kPw1 = false>
 __device__ __forceinline__ double trail_value_sel(double b, uint32_t c, const DevColony &C, const double *pw) {
     // c < 512 * kLeanPwHi: the launcher runs this kernel only for m <= that
-    const double p = __dmul_rn(pw[c & 511u], pw[512u + (c >> 9)]);
+    // (kPw1: pw is the one-table c_l^c, c <= m)
+    const double p = kPw1 ? pw[c] : __dmul_rn(pw[c & 511u], pw[512u + (c >> 9)]);
     const double one = affine(b, C.c_l, C.c_0);
     const double closed = __dadd_rn(C.tau_min, __dmul_rn(p, __dsub_rn(b, C.tau_min)));
     const double x = c >= 2u ? closed : one;
@@ -799,20 +801,34 @@ __device__ __forceinline__ void sts_if(bool p, uint32_t *ptr, uint32_t v) {
 //     next row's loads, as predicated stores without branches;
 //   * the visited mark of a candidate step is the store of the word the
 //     winning lane already loaded for its test (no second LDS).
-template <int kMode, class RNG, int kRegs>
+// kPw1 (ATOMIC, m <= kPw1Max): c_l^c from ONE shared table of m + 1 entries,
+// pw1[c] = c_l^(c mod 512) * c_l^(512 (c div 512)) -- the two-table product
+// formed once per CTA, so the values are the same -- one LDS and no DMUL on
+// the chain.  A copy's count never exceeds m within an iteration (each ant
+// bumps each copy at most once per tour; the counts are folded every iteration).
+constexpr uint32_t kPw1Max = 4096;
+template <int kMode, class RNG, int kRegs, bool kPw1 = false>
 __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
     constexpr bool kAtomic = kMode == 1;
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ double s_pw[kAtomic ? 512 + kLeanPwHi : 1];  // ATOMIC: c_l^j | c_l^(512k)
+    __shared__ double s_pw[kAtomic && !kPw1 ? 512 + kLeanPwHi : 1];  // ATOMIC: c_l^j | c_l^(512k)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int wpb = blockDim.x >> 5;
     double *scratch = reinterpret_cast<double *>(smem) + wib * 32;
     uint32_t *vis = reinterpret_cast<uint32_t *>(smem + wpb * 32 * sizeof(double)) + static_cast<size_t>(wib) * I.words;
-    if constexpr (kAtomic) {
+    double *pw1 = reinterpret_cast<double *>(
+        smem + ((wpb * (32 * sizeof(double) + I.words * sizeof(uint32_t)) + 15) & ~static_cast<size_t>(15)));
+    if constexpr (kAtomic && kPw1) {
+#pragma unroll 4
+        for (uint32_t i = threadIdx.x; i <= C.m; i += blockDim.x)
+            pw1[i] = __dmul_rn(__ldg(C.pw_lo + (i & 511u)), __ldg(C.pw_hi + (i >> 9)));
+        __syncthreads();
+    } else if constexpr (kAtomic) {
         for (uint32_t i = threadIdx.x; i < 512 + kLeanPwHi; i += blockDim.x)
             s_pw[i] = i < 512 + C.pw_hi_n ? C.pw_lo[i] : 0.0;
         __syncthreads();
     }
+    const double *pwt = kPw1 ? pw1 : s_pw;
     const uint64_t it = *C.iter;
     const uint32_t n = I.n;
     const uint32_t one = 1u;
@@ -842,7 +858,7 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             uint32_t *vw = vis + (c >> 5);
             const uint32_t word = *vw, bit = 1u << (c & 31);
             const bool unv = !(word & bit);
-            const double tv = kAtomic ? trail_value_sel(tl, cl, C, s_pw) : tl;
+            const double tv = kAtomic ? trail_value_sel<kPw1>(tl, cl, C, pwt) : tl;
             const double score = __dmul_rn(tv, __hiloint2double(static_cast<int>(el.w), static_cast<int>(el.z)));
             // off-chain: this lane's copy tauc[cur][lane] gets f(its trail) if it
             // holds the chosen slot or the late mirror copy (the slot of prev)
@@ -877,7 +893,7 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
                                   [&](uint32_t x, bool act) {
                                       if (!act) return 0.0;
                                       const size_t k = static_cast<size_t>(cur) * n + x;
-                                      return trail_value_sel(ld_relaxed(C.tau + k), ld_relaxed_u32(C.cnt + k), C, s_pw);
+                                      return trail_value_sel<kPw1>(ld_relaxed(C.tau + k), ld_relaxed_u32(C.cnt + k), C, pwt);
                                   },
                                   lane, st);
                 } else {
@@ -2263,14 +2279,15 @@ __global__ void k_island_sum(const uint32_t *const *tours, int count, uint32_t n
 
 // ============================================================ launchers
 
-static size_t construct_smem(const DevInstance &I, const DevColony &C, int wpb, bool pw) {
-    return static_cast<size_t>(wpb) * (32 * sizeof(double) + I.words * sizeof(uint32_t)) +
-           (pw ? (512 + C.pw_hi_n) * sizeof(double) : 0);
+static size_t construct_smem(const DevInstance &I, const DevColony &C, int wpb, bool pw, size_t extra = 0) {
+    const size_t base = static_cast<size_t>(wpb) * (32 * sizeof(double) + I.words * sizeof(uint32_t)) +
+                        (pw ? (512 + C.pw_hi_n) * sizeof(double) : 0);
+    return extra ? ((base + 15) & ~static_cast<size_t>(15)) + extra : base;
 }
 
 template <class K>
 static void launch_tour_kernel(K kernel, const DevInstance &I, const DevColony &C, bool one_warp,
-                               cudaStream_t s, bool pw = false) {
+                               cudaStream_t s, bool pw = false, size_t extra_smem = 0) {
     const int threads = one_warp ? 32 : kBlock;
     const int wpb = threads / 32;
     unsigned grid = one_warp ? 1u : blocks_for(C.m, wpb);
@@ -2282,7 +2299,7 @@ static void launch_tour_kernel(K kernel, const DevInstance &I, const DevColony &
         return e ? static_cast<unsigned>(std::strtoul(e, nullptr, 10)) : 0u;
     }();
     if (cap && !one_warp) grid = std::min(grid, std::max(1u, cap / wpb));
-    const size_t smem = construct_smem(I, C, wpb, pw);
+    const size_t smem = construct_smem(I, C, wpb, pw, extra_smem);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kernel<<<grid, threads, smem, s>>>(I, C);
@@ -2294,15 +2311,16 @@ static void launch_tour_kernel(K kernel, const DevInstance &I, const DevColony &
 // waves instead of four (measured: relaxed 41.9 -> 38.2, atomic 57.9 -> 49.8 ms).
 constexpr int kWideRegs = 72;
 
-template <int kMode, class RNG, int kRegs, bool kLean>
+template <int kMode, class RNG, int kRegs, bool kLean, bool kPw1 = false>
 constexpr auto dense_kernel() {
-    if constexpr (kLean) return k_tour_lean<kMode, RNG, kRegs>;
+    if constexpr (kLean) return k_tour_lean<kMode, RNG, kRegs, kPw1>;
     else return k_construct_dense<kMode, RNG, kRegs>;
 }
 
-template <int kMode, class RNG, bool kLean>
+template <int kMode, class RNG, bool kLean, bool kPw1 = false>
 static void launch_dense_t(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw) {
-    auto narrow = dense_kernel<kMode, RNG, kMaxRegs, kLean>();
+    auto narrow = dense_kernel<kMode, RNG, kMaxRegs, kLean, kPw1>();
+    const size_t extra = kPw1 ? (static_cast<size_t>(C.m) + 1) * sizeof(double) : 0;
     if (!one_warp) {
         // The narrow-vs-wide decision (occupancy query) is made once per
         // (device, shared memory, m) and remembered per host thread: it costs
@@ -2312,7 +2330,7 @@ static void launch_dense_t(const DevInstance &I, const DevColony &C, bool one_wa
         static thread_local Memo memo;
         int dev = 0;
         cudaGetDevice(&dev);
-        const size_t smem = construct_smem(I, C, kBlock / 32, pw);
+        const size_t smem = construct_smem(I, C, kBlock / 32, pw, extra);
         if (memo.dev != dev || memo.smem != smem || memo.m != C.m) {
             int sms = 0, per_sm = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2322,16 +2340,46 @@ static void launch_dense_t(const DevInstance &I, const DevColony &C, bool one_wa
             memo = Memo{dev, smem, C.m, static_cast<uint64_t>(per_sm) * sms * (kBlock / 32) < C.m};
         }
         if (memo.wide) {
-            launch_tour_kernel(dense_kernel<kMode, RNG, kWideRegs, kLean>(), I, C, false, s, pw);
+            launch_tour_kernel(dense_kernel<kMode, RNG, kWideRegs, kLean, kPw1>(), I, C, false, s, pw, extra);
             return;
         }
     }
-    launch_tour_kernel(narrow, I, C, one_warp, s, pw);
+    launch_tour_kernel(narrow, I, C, one_warp, s, pw, extra);
 }
 
 template <int kMode, class RNG>
 static void launch_dense(const DevInstance &I, const DevColony &C, bool one_warp, cudaStream_t s, bool pw = false) {
     if (C.k == 1 && C.L == 32 && !one_warp && (!pw || C.pw_hi_n <= kLeanPwHi)) {
+#ifndef ACS_NO_PW1
+        if constexpr (kMode == 1) {
+            // k_tour_lean, ATOMIC: the one-table c_l^c in shared memory, when its
+            // (m + 1) * 8 B per CTA still lets the whole colony be resident in
+            // one wave (pr2392: 19 KB, 10 CTAs per SM as without it); else the
+            // two-table build (measured: pr2392 atomic 1.554 -> 1.488 ms)
+            struct Memo { int dev = -1; uint32_t m = 0, words = 0; bool fits = false; };
+            static thread_local Memo memo;
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (memo.dev != dev || memo.m != C.m || memo.words != I.words) {
+                bool fits = false;
+                if (C.m <= kPw1Max) {
+                    auto k = dense_kernel<kMode, RNG, kMaxRegs, true, true>();
+                    const size_t smem = construct_smem(I, C, kBlock / 32, false, (static_cast<size_t>(C.m) + 1) * sizeof(double));
+                    int sms = 0, per_sm = 0;
+                    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                    if (smem > 48 * 1024)
+                        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBlock, smem);
+                    fits = static_cast<uint64_t>(per_sm) * sms * (kBlock / 32) >= C.m;
+                }
+                memo = Memo{dev, C.m, I.words, fits};
+            }
+            if (memo.fits) {
+                launch_dense_t<kMode, RNG, true, true>(I, C, one_warp, s, false);
+                return;
+            }
+        }
+#endif
         launch_dense_t<kMode, RNG, true>(I, C, one_warp, s, false);  // k_tour_lean: static power tables
         return;
     }
