@@ -576,6 +576,19 @@ __device__ __forceinline__ void red_add1(uint32_t *p) {
 
 // index of copy `lane` (0: tau[u][v], 1: tau[v][u], 2: tauc[u][pos], 3: tauc[v][mirror])
 // into the dense (n*n) or candidate (n*32) array; returns false when absent
+// ATOMIC: a dense counter cnt[a][b] is bumped only when b has no slot in a's
+// candidate row (no candidate copy of the entry is counted): the fallback
+// scans, the only readers of dense trails during construction, never look at
+// a's candidates (all visited), and the fold takes the count of such an entry
+// from its candidate copy (k_fold_counts).  One red per step instead of two.
+#ifndef ACS_DENSE_CAND_SKIP
+#define ACS_DENSE_CAND_SKIP 1
+#endif
+// skip predicate for the dense lanes of copy_index (lane 0: (u, v), lane 1:
+// (v, u)): the entry's candidate copy is bumped instead
+__device__ __forceinline__ bool dense_counted_by_cand(int lane, int pos, uint32_t mirror, uint32_t lmax) {
+    return ACS_DENSE_CAND_SKIP && (lane == 0 ? (pos >= 0 && pos < 32) : mirror < lmax);
+}
 __device__ __forceinline__ bool copy_index(uint32_t n, uint32_t u, uint32_t v, int pos,
                                            uint32_t mirror, int lane, bool &dense, size_t &idx) {
     const bool odd = lane & 1;
@@ -689,8 +702,13 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
                 size_t k;
                 // lanes 0-2 now; lane 3's copy (tauc[v][mirror]) one step late, above
                 if (lane < 3 && copy_index(n, cur, st.v, st.pos, st.mirror, lane, dense, k)) {
-                    if constexpr (kAtomic) red_add1((dense ? C.cnt : C.cntc) + k);
-                    else st_relaxed((dense ? C.tau : C.tauc) + k, affine(st.tau_old, C.c_l, C.c_0));
+                    if constexpr (kAtomic) {
+                        // lane 1's candidate copy is the late mirror one: counted iff mirror < L
+                        if (!(dense && dense_counted_by_cand(lane, st.pos, st.mirror, C.L)))
+                            red_add1((dense ? C.cnt : C.cntc) + k);
+                    } else {
+                        st_relaxed((dense ? C.tau : C.tauc) + k, affine(st.tau_old, C.c_l, C.c_0));
+                    }
                 }
                 mprev = cur;
             }
@@ -727,7 +745,8 @@ __global__ void __maxnreg__(kRegs) k_construct_dense(DevInstance I, DevColony C)
             size_t k;
             if (copy_index(n, cur, start, pos, mirror, lane, dense, k)) {
                 if constexpr (kAtomic) {
-                    red_add1((dense ? C.cnt : C.cntc) + k);
+                    if (!(dense && dense_counted_by_cand(lane, pos, mirror, 32u)))
+                        red_add1((dense ? C.cnt : C.cntc) + k);
                 } else {
                     const double told = ld_relaxed(C.tau + static_cast<size_t>(cur) * n + start);
                     st_relaxed((dense ? C.tau : C.tauc) + k, affine(told, C.c_l, C.c_0));
@@ -869,6 +888,7 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             const double told = tl;  // the value this lane's update read (tl is reloaded below)
 #endif
             const int32_t dl = static_cast<int32_t>(el.y);
+            const bool nomir = (el.x >> 24) == kNoMirror;  // this slot's node has no slot for cur
             int pos;
             uint32_t v;
             bool cand;
@@ -908,8 +928,11 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
                 // the non-candidate edge's dense copies: lane 0 tau[u][v], lane 1 tau[v][u]
                 if (lane < 2) {
                     const size_t di = lane ? static_cast<size_t>(v) * n + cur : static_cast<size_t>(cur) * n + v;
-                    if constexpr (kAtomic) red_add1(C.cnt + di);
-                    else st_relaxed(C.tau + di, affine(st.tau_old, C.c_l, C.c_0));
+                    if constexpr (kAtomic) {
+                        if (!(lane == 1 && dense_counted_by_cand(1, -1, st.mirror, 32u))) red_add1(C.cnt + di);
+                    } else {
+                        st_relaxed(C.tau + di, affine(st.tau_old, C.c_l, C.c_0));
+                    }
                 }
                 if (lane == 0) {
                     vis[v >> 5] |= 1u << (v & 31);
@@ -939,11 +962,17 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             auto update_stores = [&]() {
                 if constexpr (kAtomic) {
                     red_add_if(me || mw, C.cntc + mi, one);
+#if ACS_DENSE_CAND_SKIP
+                    // dense counters: (cur, v) has its candidate copy; (v, cur)
+                    // only when cur is not in v's row (no late mirror copy)
+                    red_add_if(me && nomir, C.cnt + (static_cast<size_t>(v) * n + cur), one);
+#else
                     // the two dense counters in one instruction: lane pos bumps
                     // cnt[u][v], lane pos ^ 1 bumps cnt[v][u] (no value to move)
                     const bool mate = lane == (pos ^ 1);
                     const uint32_t row = me ? cur : v;
                     red_add_if(pos >= 0 && (me || mate), C.cnt + (static_cast<size_t>(row) * n + (cur ^ v ^ row)), one);
+#endif
                 } else {
                     const size_t d_uv = static_cast<size_t>(cur) * n + v, d_vu = static_cast<size_t>(v) * n + cur;
 #ifdef ACS_COUNT_LOST
@@ -1006,7 +1035,8 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
         size_t k;
         if (copy_index(n, cur, start, pos, mirror, lane, dense, k)) {
             if constexpr (kAtomic) {
-                red_add1((dense ? C.cnt : C.cntc) + k);
+                if (!(dense && dense_counted_by_cand(lane, pos, mirror, 32u)))
+                    red_add1((dense ? C.cnt : C.cntc) + k);
             } else {
                 const double told = ld_relaxed(C.tau + static_cast<size_t>(cur) * n + start);
                 st_relaxed((dense ? C.tau : C.tauc) + k, affine(told, C.c_l, C.c_0));
@@ -1053,6 +1083,12 @@ __global__ void k_fold_counts(DevColony C, size_t dense_count, size_t cand_count
         if (c) {
             C.tauc[i] = trail_value(C.tauc[i], c, C, C.pw_lo, C.pw_hi);
             C.cntc[i] = 0;
+#if ACS_DENSE_CAND_SKIP
+            // the dense copy of the same entry was not counted: same count
+            const uint32_t b = C.rows[i].x & kIdMask;
+            const size_t di = (i / 32) * (cand_count / 32) + b;
+            C.tau[di] = trail_value(C.tau[di], c, C, C.pw_lo, C.pw_hi);
+#endif
         }
     }
 }
