@@ -387,24 +387,28 @@ struct PhiloxWarp {
     Philox key;         // (seed, iteration, ant); key.draw unused
     uint64_t q0_k;
     uint64_t mine;      // draw base + lane
-    uint32_t base, draw, qmask;
+    uint32_t base;      // first draw of the current block of 32
+    uint32_t off;       // draws consumed in this block
+    uint32_t qsh;       // the block's greedy-test ballot shifted by off: bit 0 = next draw's
 
     __device__ __forceinline__ void fill() {
         Philox p = key;
         p.draw = base + (threadIdx.x & 31u);
         mine = p.peek();
-        qmask = __ballot_sync(kFull, (mine >> 11) <= q0_k);
+        qsh = __ballot_sync(kFull, (mine >> 11) <= q0_k);
     }
     __device__ __forceinline__ void derive(uint64_t seed, uint64_t it, uint64_t a, uint64_t q0k) {
         key.derive(seed, it, a);
         q0_k = q0k;
-        base = draw = 0;
+        base = off = 0;
         fill();
     }
-    __device__ __forceinline__ uint64_t peek() const { return shfl_u64(mine, static_cast<int>(draw - base)); }
+    __device__ __forceinline__ uint64_t peek() const { return shfl_u64(mine, static_cast<int>(off)); }
     __device__ __forceinline__ void advance() {
-        if (++draw - base == 32u) {  // warp-uniform, once per 32 draws
+        qsh >>= 1;
+        if (++off == 32u) {  // warp-uniform, once per 32 draws
             base += 32u;
+            off = 0;
             fill();
         }
     }
@@ -413,7 +417,7 @@ struct PhiloxWarp {
         advance();
         return r;
     }
-    __device__ __forceinline__ bool greedy_bit() const { return (qmask >> (draw - base)) & 1u; }
+    __device__ __forceinline__ bool greedy_bit() const { return qsh & 1u; }
 };
 
 template <>
