@@ -886,7 +886,9 @@ __global__ void __maxnreg__(kRegs) k_tour_lean(DevInstance I, DevColony C) {
             // off-chain: this lane's copy tauc[cur][lane] gets f(its trail) if it
             // holds the chosen slot or the late mirror copy (the slot of prev)
             const bool mw = c == mprev;
-            const size_t mi = static_cast<size_t>(cur) * 32 + lane;
+            // ATOMIC reuses the index row cur was loaded with (ri = cur * 32 + lane);
+            // RELAXED recomputes it (reusing it there measured 3 % slower: spills)
+            const size_t mi = kAtomic ? ri : static_cast<size_t>(cur) * 32 + lane;
             const double mval = kAtomic ? 0.0 : affine(tl, C.c_l, C.c_0);
 #ifdef ACS_COUNT_LOST
             const double told = tl;  // the value this lane's update read (tl is reloaded below)
