@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include <cooperative_groups.h>
+#include <type_traits>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "../../include/acs_gpu.h"
@@ -226,6 +227,34 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
         // fallback that walks the whole list pays ceil(slices / kExtBatch)
         // pairs of dependent L2 trips instead of one pair per slice)
         constexpr uint32_t kExtBatch = kDefer ? ACS_EXT_BATCH_DEFER : ACS_EXT_BATCH;
+        if constexpr (kExtBatch == 1) {  // one slice per trip (the free-running kernels)
+        for (uint32_t base = 0; base < C.ext_len; base += 32) {
+            if (base) q = __ldg(xrow + base + lane);
+            const bool in_list = q.x != kEmpty;
+            const uint32_t qid = q.x & kIdMask;
+            const bool act = in_list && !visited(vis, qid);
+            const double tv = tau_of(in_list ? qid : 0u, act);
+            if (act) {
+                const double sc = __dmul_rn(tv, __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z)));
+                if (!have || sc > bs || (sc == bs && qid < bv)) {
+                    have = true; bs = sc; bv = qid; bt = tv; bm = q.x >> 24;
+                }
+            }
+            double sb = bs;
+            uint32_t node = have ? bv : 0xffffffffu;
+            warp_argmax_node(sb, node, have);
+            // the list ends inside this slice: every non-candidate node was scanned
+            const bool exhausted = __any_sync(kFull, !in_list);
+            const uint32_t lw = __shfl_sync(kFull, q.w, 31), lz = __shfl_sync(kFull, q.z, 31);
+            const double bound = __dmul_rn(C.tau_bound, __hiloint2double(static_cast<int>(lw), static_cast<int>(lz)));
+            if (node != 0xffffffffu && (exhausted || bound < sb)) {
+                const unsigned owner = __ballot_sync(kFull, have && bv == node);
+                const int src = __ffs(owner) - 1;
+                finish_scan(I, C, cur, node, __shfl_sync(kFull, bt, src), lane, o, __shfl_sync(kFull, bm, src));
+                return;
+            }
+        }
+        } else {
         for (uint32_t base = 0; base < C.ext_len; base += 32 * kExtBatch) {
             uint4 qs[kExtBatch];
             qs[0] = base ? __ldg(xrow + base + lane) : q;
@@ -268,6 +297,7 @@ __device__ __forceinline__ void fallback_scan(const DevInstance &I, const DevCol
                 }
                 if (base + 32 * j < C.ext_len) q = qj;  // the ring stage starts past the last slice
             }
+        }
         }
         // Past the ext rows: rings of grid cells around cur, nearest first.
         // Every node closer than the last ext entry is a candidate or an ext
@@ -434,6 +464,54 @@ __device__ __forceinline__ void rng_init(RNG &rng, const DevColony &C, uint64_t 
 }
 template <>
 __device__ __forceinline__ void rng_init(PhiloxWarp &rng, const DevColony &C, uint64_t it, uint64_t a) {
+    rng.derive(C.seed, it, a, C.q0_k);
+}
+
+// PhiloxWarp with the round-1 bookkeeping (the ballot shifted by the draw
+// offset at every test).  The pre-shifted form is faster in every 96-register
+// build but 8 % slower in the 72-register RELAXED build of multi-wave colonies
+// (rnd10k: 25.9 vs 28.1 ms, where it changes what ptxas spills), so that one
+// instantiation keeps this form.  Identical draws.
+struct PhiloxWarpU {  // the same stream with an unshifted ballot (see below)
+    Philox key;         // (seed, iteration, ant); key.draw unused
+    uint64_t q0_k;
+    uint64_t mine;      // draw base + lane
+    uint32_t base, draw, qmask;
+
+    __device__ __forceinline__ void fill() {
+        Philox p = key;
+        p.draw = base + (threadIdx.x & 31u);
+        mine = p.peek();
+        qmask = __ballot_sync(kFull, (mine >> 11) <= q0_k);
+    }
+    __device__ __forceinline__ void derive(uint64_t seed, uint64_t it, uint64_t a, uint64_t q0k) {
+        key.derive(seed, it, a);
+        q0_k = q0k;
+        base = draw = 0;
+        fill();
+    }
+    __device__ __forceinline__ uint64_t peek() const { return shfl_u64(mine, static_cast<int>(draw - base)); }
+    __device__ __forceinline__ void advance() {
+        if (++draw - base == 32u) {  // warp-uniform, once per 32 draws
+            base += 32u;
+            fill();
+        }
+    }
+    __device__ __forceinline__ uint64_t next() {
+        const uint64_t r = peek();
+        advance();
+        return r;
+    }
+    __device__ __forceinline__ bool greedy_bit() const { return (qmask >> (draw - base)) & 1u; }
+};
+template <>
+struct Lookahead<PhiloxWarpU> {
+    bool g;
+    __device__ __forceinline__ void prepare(const PhiloxWarpU &rng) { g = rng.greedy_bit(); }
+    __device__ __forceinline__ bool greedy(const DevColony &) const { return g; }
+};
+template <>
+__device__ __forceinline__ void rng_init(PhiloxWarpU &rng, const DevColony &C, uint64_t it, uint64_t a) {
     rng.derive(C.seed, it, a, C.q0_k);
 }
 
@@ -2355,7 +2433,9 @@ constexpr int kWideRegs = 72;
 
 template <int kMode, class RNG, int kRegs, bool kLean, bool kPw1 = false>
 constexpr auto dense_kernel() {
-    if constexpr (kLean) return k_tour_lean<kMode, RNG, kRegs, kPw1>;
+    if constexpr (kLean && kMode == 0 && kRegs == kWideRegs && std::is_same_v<RNG, PhiloxWarp>)
+        return k_tour_lean<kMode, PhiloxWarpU, kRegs, kPw1>;  // see PhiloxWarpU
+    else if constexpr (kLean) return k_tour_lean<kMode, RNG, kRegs, kPw1>;
     else return k_construct_dense<kMode, RNG, kRegs>;
 }
 
